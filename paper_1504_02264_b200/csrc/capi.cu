@@ -1,0 +1,747 @@
+// C ABI of the B200 DPRI-LES library (declared in include/les_b200.h).
+//
+// A domain handle owns device-resident state: u, v, w (plus a second
+// velocity set the fused step kernels ping-pong through), p (plus a second
+// buffer for the twinned scheme), rhs, mask, fgh, fgh_old, spacings and SOR
+// coefficients.  One time step is captured once into a CUDA graph per
+// (n_iter, scheme, omega) and replayed.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "les_b200.h"
+#include "lesb_common.cuh"
+#include "lesb_kernels.h"
+
+using namespace lesb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return fail(LESB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+enum { MODE_SYNC = 0, MODE_ASYNC = 1 };
+
+// device-side step bookkeeping for asynchronous runs
+struct StepBook {
+  unsigned flags;       // stage bits of the current (or first failing) step
+  unsigned steps;       // steps enqueued and completed on the device
+  int fail_step;        // -1 while no step failed
+  unsigned fail_flags;  // stage bits of the first failing step
+};
+
+__global__ void k_step_tail(StepBook* b) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (b->flags && b->fail_step < 0) {
+      b->fail_step = (int)b->steps;
+      b->fail_flags = b->flags;
+    }
+    b->steps += 1;
+  }
+}
+
+int first_stage(unsigned bits) {
+  for (int s = 0; s < 7; ++s)
+    if (bits & (1u << s)) return s;
+  return -1;
+}
+
+}  // namespace
+
+struct lesb_domain {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  Geo g{};
+  float dt = 0.5f, vn = 1e-5f, cs = 0.14f, csd2s = 0.f;
+  float* csd2 = nullptr;
+  float *dx1 = nullptr, *dy1 = nullptr, *dzn = nullptr;
+  float *u = nullptr, *v = nullptr, *w = nullptr, *ub = nullptr, *vb = nullptr, *wb = nullptr;
+  float *p = nullptr, *pb = nullptr, *rhs = nullptr, *mask = nullptr, *fgh = nullptr, *fgh_old = nullptr;
+  float* cn1 = nullptr;
+  float* cn[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  float cn1s = 0.f;
+  bool coeffs_set = false;
+  float* inflow_d = nullptr;
+  float* inflow_h = nullptr;  // pinned
+  StepBook* book_d = nullptr;
+  StepBook* book_h = nullptr;  // pinned
+  double* partials = nullptr;
+  long long partials_cap = 0;
+  double* res_d = nullptr;
+  double* res_h = nullptr;  // pinned
+  int res_cap = 0;
+  float* scratch = nullptr;  // im*jm*km
+  std::map<std::tuple<int, int, int, unsigned>, cudaGraphExec_t> graphs;
+  bool known_finite = false;
+  long long n_alloc = 0;  // (im+3)*si
+  long long n_py = 0;     // (im+2)*si : the Python-visible array
+  std::mutex mu;
+
+  Spac spac() const { return Spac{dx1, dy1, dzn}; }
+  SorC sorc() const { return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5]}; }
+  long long n_int() const { return (long long)g.im * g.jm * g.km; }
+};
+
+namespace {
+
+int ensure_partials(lesb_domain* h, int n_iter) {
+  long long need = (long long)n_iter * 2 * std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g));
+  if (need > h->partials_cap) {
+    if (h->partials) cudaFree(h->partials);
+    h->partials = nullptr;
+    CK(cudaMalloc(&h->partials, need * sizeof(double)));
+    h->partials_cap = need;
+  }
+  if (n_iter > h->res_cap) {
+    if (h->res_d) cudaFree(h->res_d);
+    if (h->res_h) cudaFreeHost(h->res_h);
+    h->res_d = nullptr;
+    h->res_h = nullptr;
+    CK(cudaMalloc(&h->res_d, n_iter * sizeof(double)));
+    CK(cudaMallocHost(&h->res_h, n_iter * sizeof(double)));
+    h->res_cap = n_iter;
+  }
+  return LESB_OK;
+}
+
+void clear_graphs(lesb_domain* h) {
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+}
+
+float* field_ptr(lesb_domain* h, int f) {
+  switch (f) {
+    case LESB_U: return h->u;
+    case LESB_V: return h->v;
+    case LESB_W: return h->w;
+    case LESB_P: return h->p;
+    case LESB_MASK: return h->mask;
+    case LESB_FGH: return h->fgh;
+    case LESB_FGH_OLD: return h->fgh_old;
+    case LESB_RHS: return h->rhs;
+    default: return nullptr;
+  }
+}
+
+long long field_count(lesb_domain* h, int f) { return (f == LESB_FGH || f == LESB_FGH_OLD) ? 3 * h->n_py : h->n_py; }
+
+// Enqueue the press stage on the stream: rhs = div(u)/dt, SOR, final halo.
+void enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, bool rhs_from_state, unsigned* flags) {
+  if (rhs_from_state) launch_divergence(h->g, h->spac(), h->u, h->v, h->w, h->rhs, h->dt, 1, h->st);
+  enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d, flags, h->st,
+              nullptr);
+}
+
+// The full step: velnw+bondv1 (A -> B), velfg+feedbf+les+adam+rhs (B -> A), press.
+void enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omega) {
+  unsigned* flags = &h->book_d->flags;
+  launch_velnw_bondv1(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->inflow_d, h->ub, h->vb, h->wb,
+                      flags, h->st);
+  launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
+                   h->vn, h->dt, h->cs != 0.0f, h->csd2, h->csd2s, flags, h->st);
+  enqueue_press(h, n_iter, scheme, omega, false, flags);
+}
+
+int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cudaGraphExec_t* out) {
+  unsigned ob;
+  std::memcpy(&ob, &omega, 4);
+  auto key = std::make_tuple(mode, n_iter, scheme, ob);
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) {
+    *out = it->second;
+    return LESB_OK;
+  }
+  int rc = ensure_partials(h, n_iter);
+  if (rc) return rc;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  if (mode == MODE_SYNC) {
+    cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), h->st);
+    cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * h->g.km * sizeof(float), cudaMemcpyHostToDevice, h->st);
+  }
+  enqueue_step_body(h, n_iter, scheme, omega);
+  if (mode == MODE_SYNC) {
+    cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st);
+    cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st);
+  } else {
+    k_step_tail<<<1, 32, 0, h->st>>>(h->book_d);
+  }
+  cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+  if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  cudaGraphExec_t exec;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  h->graphs[key] = exec;
+  *out = exec;
+  return LESB_OK;
+}
+
+// Full finiteness scan of the six state fields (les.py:387-390).
+int scan_finite(lesb_domain* h, bool* ok) {
+  CK(cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), h->st));
+  unsigned* fl = &h->book_d->flags;
+  launch_check_finite(h->u, h->n_py, fl, 1, h->st);
+  launch_check_finite(h->v, h->n_py, fl, 1, h->st);
+  launch_check_finite(h->w, h->n_py, fl, 1, h->st);
+  launch_check_finite(h->p, h->n_py, fl, 1, h->st);
+  launch_check_finite(h->fgh, 3 * h->n_py, fl, 1, h->st);
+  launch_check_finite(h->fgh_old, 3 * h->n_py, fl, 1, h->st);
+  CK(cudaMemcpyAsync(&h->book_h->flags, fl, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  *ok = h->book_h->flags == 0;
+  return LESB_OK;
+}
+
+int check_args_step(lesb_domain* h, int n_iter, int scheme) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  if (n_iter < 1) return fail(LESB_E_ARG, "n_iter must be >= 1");
+  if (scheme != LESB_REDBLACK && scheme != LESB_TWINNED) return fail(LESB_E_ARG, "unknown scheme");
+  if (!h->coeffs_set) return fail(LESB_E_STATE, "SOR coefficients not set (lesb_set_coeffs)");
+  return LESB_OK;
+}
+
+// Reference behaviour when the state already holds a non-finite value: velnw
+// runs and the check after it raises (velnw can never clear a non-finite).
+int handle_dirty_state(lesb_domain* h, int* fail_stage, bool* failed) {
+  *failed = false;
+  if (h->known_finite) return LESB_OK;
+  bool ok = false;
+  int rc = scan_finite(h, &ok);
+  if (rc) return rc;
+  if (!ok) {
+    launch_velnw(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->st);
+    CK(cudaStreamSynchronize(h->st));
+    if (fail_stage) *fail_stage = LESB_STAGE_VELNW;
+    *failed = true;
+  }
+  h->known_finite = ok;
+  return LESB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lesb_last_error(void) { return g_err.c_str(); }
+int lesb_abi_version(void) { return LESB_ABI_VERSION; }
+
+int lesb_create(const lesb_desc* d, lesb_handle* out) {
+  if (!d || !out) return fail(LESB_E_ARG, "null argument");
+  if (d->im < 1 || d->jm < 1 || d->km < 1) return fail(LESB_E_ARG, "grid dimensions must be >= 1");
+  if (!d->dx1 || !d->dy1 || !d->dzn) return fail(LESB_E_ARG, "spacing arrays are required");
+  auto* h = new lesb_domain();
+  h->device = d->device;
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(LESB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  Geo& g = h->g;
+  g.im = d->im;
+  g.jm = d->jm;
+  g.km = d->km;
+  g.sj = d->km + 2;
+  g.si = (long long)(d->jm + 2) * (d->km + 2);
+  g.ioff = d->i_offset;
+  g.west_bc = d->west_boundary ? 1 : 0;
+  g.east_bc = d->east_boundary ? 1 : 0;
+  h->n_py = (long long)(g.im + 2) * g.si;
+  h->n_alloc = (long long)(g.im + 3) * g.si;
+  h->dt = d->dt;
+  h->vn = d->vn;
+  h->cs = d->cs;
+  h->csd2s = d->csd2_scalar;
+  const size_t fb = h->n_alloc * sizeof(float);
+  cudaError_t err = cudaSuccess;
+  auto A = [&](float** ptr, size_t bytes) {
+    if (err == cudaSuccess) err = cudaMalloc(ptr, bytes);
+    if (err == cudaSuccess) err = cudaMemset(*ptr, 0, bytes);
+  };
+  A(&h->u, fb); A(&h->v, fb); A(&h->w, fb);
+  A(&h->ub, fb); A(&h->vb, fb); A(&h->wb, fb);
+  A(&h->p, fb); A(&h->pb, fb); A(&h->rhs, fb); A(&h->mask, fb);
+  A(&h->fgh, 3 * fb); A(&h->fgh_old, 3 * fb);
+  A(&h->dx1, (g.im + 3) * sizeof(float));
+  A(&h->dy1, (g.jm + 2) * sizeof(float));
+  A(&h->dzn, (g.km + 2) * sizeof(float));
+  A(&h->inflow_d, 3 * g.km * sizeof(float));
+  A(&h->scratch, h->n_int() * sizeof(float));
+  if (err == cudaSuccess) err = cudaMalloc(&h->book_d, sizeof(StepBook));
+  if (err == cudaSuccess) err = cudaMallocHost(&h->book_h, sizeof(StepBook));
+  if (err == cudaSuccess) err = cudaMallocHost(&h->inflow_h, 3 * g.km * sizeof(float));
+  if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaMemcpy(h->dx1, d->dx1, (g.im + 3) * sizeof(float), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMemcpy(h->dy1, d->dy1, (g.jm + 2) * sizeof(float), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMemcpy(h->dzn, d->dzn, (g.km + 2) * sizeof(float), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) {
+    StepBook b{0u, 0u, -1, 0u};
+    err = cudaMemcpy(h->book_d, &b, sizeof(b), cudaMemcpyHostToDevice);
+  }
+  if (err == cudaSuccess && d->csd2) {
+    err = cudaMalloc(&h->csd2, h->n_int() * sizeof(float));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(h->csd2, d->csd2, h->n_int() * sizeof(float), cudaMemcpyHostToDevice);
+  }
+  if (err != cudaSuccess) {
+    std::string m = std::string("lesb_create: ") + cudaGetErrorString(err);
+    lesb_destroy(h);
+    return fail(err == cudaErrorMemoryAllocation ? LESB_E_NOMEM : LESB_E_CUDA, m);
+  }
+  h->known_finite = true;  // all zero
+  *out = h;
+  return LESB_OK;
+}
+
+int lesb_destroy(lesb_handle h) {
+  if (!h) return LESB_OK;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  clear_graphs(h);
+  float* bufs[] = {h->u, h->v, h->w, h->ub, h->vb, h->wb, h->p, h->pb, h->rhs, h->mask, h->fgh, h->fgh_old,
+                   h->dx1, h->dy1, h->dzn, h->inflow_d, h->scratch, h->csd2, h->cn1,
+                   h->cn[0], h->cn[1], h->cn[2], h->cn[3], h->cn[4], h->cn[5]};
+  for (float* b : bufs)
+    if (b) cudaFree(b);
+  if (h->partials) cudaFree(h->partials);
+  if (h->res_d) cudaFree(h->res_d);
+  if (h->book_d) cudaFree(h->book_d);
+  if (h->res_h) cudaFreeHost(h->res_h);
+  if (h->book_h) cudaFreeHost(h->book_h);
+  if (h->inflow_h) cudaFreeHost(h->inflow_h);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+  return LESB_OK;
+}
+
+int lesb_set_coeffs(lesb_handle h, const lesb_coeffs* c) {
+  if (!h || !c) return fail(LESB_E_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  const Geo& g = h->g;
+  const int lens[6] = {g.im, g.im, g.jm, g.jm, g.km, g.km};
+  const float* src[6] = {c->cn2l, c->cn2s, c->cn3l, c->cn3s, c->cn4l, c->cn4s};
+  for (int a = 0; a < 6; ++a) {
+    if (!src[a]) return fail(LESB_E_ARG, "cn2l/cn2s/cn3l/cn3s/cn4l/cn4s are required");
+    if (!h->cn[a]) CK(cudaMalloc(&h->cn[a], lens[a] * sizeof(float)));
+    CK(cudaMemcpy(h->cn[a], src[a], lens[a] * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  if (c->cn1) {
+    if (!h->cn1) CK(cudaMalloc(&h->cn1, h->n_int() * sizeof(float)));
+    CK(cudaMemcpy(h->cn1, c->cn1, h->n_int() * sizeof(float), cudaMemcpyHostToDevice));
+  } else if (h->cn1) {
+    cudaFree(h->cn1);
+    h->cn1 = nullptr;
+  }
+  h->cn1s = c->cn1_scalar;
+  h->coeffs_set = true;
+  clear_graphs(h);
+  return LESB_OK;
+}
+
+int lesb_set_physics(lesb_handle h, float dt, float vn, float cs, const float* csd2, float csd2_scalar) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  h->dt = dt;
+  h->vn = vn;
+  h->cs = cs;
+  h->csd2s = csd2_scalar;
+  if (csd2) {
+    if (!h->csd2) CK(cudaMalloc(&h->csd2, h->n_int() * sizeof(float)));
+    CK(cudaMemcpy(h->csd2, csd2, h->n_int() * sizeof(float), cudaMemcpyHostToDevice));
+  } else if (h->csd2) {
+    cudaFree(h->csd2);
+    h->csd2 = nullptr;
+  }
+  clear_graphs(h);
+  return LESB_OK;
+}
+
+int lesb_upload(lesb_handle h, int field, const float* host) {
+  if (!h || !host) return fail(LESB_E_ARG, "null argument");
+  float* d = field_ptr(h, field);
+  if (!d) return fail(LESB_E_ARG, "unknown field id");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(d, host, field_count(h, field) * sizeof(float), cudaMemcpyHostToDevice));
+  if (field != LESB_MASK && field != LESB_RHS) h->known_finite = false;
+  return LESB_OK;
+}
+
+int lesb_download(lesb_handle h, int field, float* host) {
+  if (!h || !host) return fail(LESB_E_ARG, "null argument");
+  float* d = field_ptr(h, field);
+  if (!d) return fail(LESB_E_ARG, "unknown field id");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(host, d, field_count(h, field) * sizeof(float), cudaMemcpyDeviceToHost));
+  return LESB_OK;
+}
+
+void* lesb_device_ptr(lesb_handle h, int field) { return h ? (void*)field_ptr(h, field) : nullptr; }
+void* lesb_stream(lesb_handle h) { return h ? (void*)h->st : nullptr; }
+
+int lesb_synchronize(lesb_handle h) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+int lesb_check_finite(lesb_handle h, int* all_finite) {
+  if (!h || !all_finite) return fail(LESB_E_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  bool ok = false;
+  int rc = scan_finite(h, &ok);
+  if (rc) return rc;
+  *all_finite = ok ? 1 : 0;
+  h->known_finite = ok;
+  return LESB_OK;
+}
+
+// ---- single stages ----
+#define STAGE_PROLOGUE()                      \
+  if (!h) return fail(LESB_E_ARG, "null handle"); \
+  std::lock_guard<std::mutex> lk(h->mu);      \
+  CK(cudaSetDevice(h->device));
+
+#define STAGE_EPILOGUE()                      \
+  CK(cudaGetLastError());                     \
+  CK(cudaStreamSynchronize(h->st));           \
+  h->known_finite = false;                    \
+  return LESB_OK;
+
+int lesb_velnw(lesb_handle h) {
+  STAGE_PROLOGUE();
+  launch_velnw(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_bondv1(lesb_handle h, const float* in_u, const float* in_v, const float* in_w) {
+  STAGE_PROLOGUE();
+  if (!in_u || !in_v || !in_w) return fail(LESB_E_ARG, "inflow arrays are required");
+  const int km = h->g.km;
+  std::memcpy(h->inflow_h, in_u, km * sizeof(float));
+  std::memcpy(h->inflow_h + km, in_v, km * sizeof(float));
+  std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
+  CK(cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * km * sizeof(float), cudaMemcpyHostToDevice, h->st));
+  launch_bondv1(h->g, h->u, h->v, h->w, h->inflow_d, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_velfg(lesb_handle h) {
+  STAGE_PROLOGUE();
+  launch_velfg(h->g, h->spac(), h->u, h->v, h->w, h->fgh, h->vn, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_feedbf(lesb_handle h) {
+  STAGE_PROLOGUE();
+  launch_feedbf(h->g, h->u, h->v, h->w, h->fgh, h->mask, h->dt, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_les_viscosity(lesb_handle h) {
+  STAGE_PROLOGUE();
+  if (h->cs != 0.0f) launch_les(h->g, h->spac(), h->u, h->v, h->w, h->fgh, h->csd2, h->csd2s, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_adam(lesb_handle h) {
+  STAGE_PROLOGUE();
+  launch_adam(h->fgh, h->fgh_old, 3 * h->n_py, h->st);
+  STAGE_EPILOGUE();
+}
+
+int lesb_divergence(lesb_handle h, float* out_host) {
+  STAGE_PROLOGUE();
+  if (!out_host) return fail(LESB_E_ARG, "null output");
+  launch_divergence(h->g, h->spac(), h->u, h->v, h->w, h->scratch, 1.0f, 0, h->st);
+  CK(cudaMemcpyAsync(out_host, h->scratch, h->n_int() * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+int lesb_strain_magnitude(lesb_handle h, float* out_host) {
+  STAGE_PROLOGUE();
+  if (!out_host) return fail(LESB_E_ARG, "null output");
+  launch_strain(h->g, h->spac(), h->u, h->v, h->w, h->scratch, h->st);
+  CK(cudaMemcpyAsync(out_host, h->scratch, h->n_int() * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* residuals_out) {
+  int rc = check_args_step(h, n_iter, scheme);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  rc = ensure_partials(h, n_iter);
+  if (rc) return rc;
+  enqueue_press(h, n_iter, scheme, omega, true, nullptr);
+  CK(cudaGetLastError());
+  if (residuals_out)
+    CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->known_finite = false;
+  return LESB_OK;
+}
+
+// ---- the time step ----
+int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* in_w, int n_iter, int scheme,
+              float omega, double* residuals_out, int* fail_stage) {
+  int rc = check_args_step(h, n_iter, scheme);
+  if (rc) return rc;
+  if (!in_u || !in_v || !in_w) return fail(LESB_E_ARG, "inflow arrays are required");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  if (fail_stage) *fail_stage = -1;
+  bool failed = false;
+  rc = handle_dirty_state(h, fail_stage, &failed);
+  if (rc) return rc;
+  if (failed) return LESB_NONFINITE;
+  cudaGraphExec_t ge;
+  rc = get_graph(h, MODE_SYNC, n_iter, scheme, omega, &ge);
+  if (rc) return rc;
+  const int km = h->g.km;
+  std::memcpy(h->inflow_h, in_u, km * sizeof(float));
+  std::memcpy(h->inflow_h + km, in_v, km * sizeof(float));
+  std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
+  CK(cudaGraphLaunch(ge, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (residuals_out) std::memcpy(residuals_out, h->res_h, n_iter * sizeof(double));
+  unsigned bits = h->book_h->flags;
+  if (bits) {
+    h->known_finite = false;
+    if (fail_stage) *fail_stage = first_stage(bits);
+    return LESB_NONFINITE;
+  }
+  return LESB_OK;
+}
+
+int lesb_set_inflow(lesb_handle h, const float* in_u, const float* in_v, const float* in_w) {
+  if (!h || !in_u || !in_v || !in_w) return fail(LESB_E_ARG, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  const int km = h->g.km;
+  CK(cudaMemcpyAsync(h->inflow_d, in_u, km * sizeof(float), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->inflow_d + km, in_v, km * sizeof(float), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->inflow_d + 2 * km, in_w, km * sizeof(float), cudaMemcpyHostToDevice, h->st));
+  return LESB_OK;
+}
+
+int lesb_step_async(lesb_handle h, int n_iter, int scheme, float omega) {
+  int rc = check_args_step(h, n_iter, scheme);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  if (!h->known_finite) {
+    bool failed = false;
+    rc = handle_dirty_state(h, nullptr, &failed);
+    if (rc) return rc;
+    if (failed) return fail(LESB_E_STATE, "state holds non-finite values");
+    StepBook b{0u, 0u, -1, 0u};
+    CK(cudaMemcpyAsync(h->book_d, &b, sizeof(b), cudaMemcpyHostToDevice, h->st));
+  }
+  cudaGraphExec_t ge;
+  rc = get_graph(h, MODE_ASYNC, n_iter, scheme, omega, &ge);
+  if (rc) return rc;
+  CK(cudaGraphLaunch(ge, h->st));
+  return LESB_OK;
+}
+
+int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_stage) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(h->book_h, h->book_d, sizeof(StepBook), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  const StepBook b = *h->book_h;
+  if (steps_done) *steps_done = (int)b.steps;
+  if (fail_step) *fail_step = b.fail_step;
+  if (fail_stage) *fail_stage = b.fail_step >= 0 ? first_stage(b.fail_flags) : -1;
+  // reset the counters for the next run
+  StepBook z{0u, 0u, -1, 0u};
+  CK(cudaMemcpyAsync(h->book_d, &z, sizeof(z), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (b.fail_step >= 0) h->known_finite = false;
+  return LESB_OK;
+}
+
+int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profiles, int n_iter, int scheme,
+                   float omega, int* steps_done, int* fail_stage) {
+  if (!h || !inflow || n_profiles < 1 || n_steps < 0) return fail(LESB_E_ARG, "bad argument");
+  int rc = check_args_step(h, n_iter, scheme);
+  if (rc) return rc;
+  const int km = h->g.km;
+  float* prof_d = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    CK(cudaSetDevice(h->device));
+    CK(cudaMalloc(&prof_d, (size_t)n_profiles * 3 * km * sizeof(float)));
+    CK(cudaMemcpyAsync(prof_d, inflow, (size_t)n_profiles * 3 * km * sizeof(float), cudaMemcpyHostToDevice,
+                       h->st));
+  }
+  int done = 0;
+  for (int s = 0; s < n_steps; ++s) {
+    const int pi = s < n_profiles ? s : n_profiles - 1;
+    if (s == 0 || n_profiles > 1) {
+      std::lock_guard<std::mutex> lk(h->mu);
+      CK(cudaMemcpyAsync(h->inflow_d, prof_d + (size_t)pi * 3 * km, 3 * km * sizeof(float),
+                         cudaMemcpyDeviceToDevice, h->st));
+    }
+    rc = lesb_step_async(h, n_iter, scheme, omega);
+    if (rc) {
+      cudaFree(prof_d);
+      return rc;
+    }
+  }
+  int fstep = -1, fstage = -1;
+  rc = lesb_poll_failure(h, &done, &fstep, &fstage);
+  cudaFree(prof_d);
+  if (rc) return rc;
+  if (fstep >= 0) {
+    if (steps_done) *steps_done = fstep;
+    if (fail_stage) *fail_stage = fstage;
+    return LESB_NONFINITE;
+  }
+  if (steps_done) *steps_done = done;
+  if (fail_stage) *fail_stage = -1;
+  return LESB_OK;
+}
+
+int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1);
+}
+
+// ---- solver on host buffers ----
+}  // extern "C"
+
+namespace {
+
+std::mutex g_solver_mu;
+std::map<std::tuple<int, int, int, int>, lesb_domain*> g_solvers;
+
+int get_solver(int im, int jm, int km, int device, lesb_domain** out) {
+  std::lock_guard<std::mutex> lk(g_solver_mu);
+  auto key = std::make_tuple(im, jm, km, device);
+  auto it = g_solvers.find(key);
+  if (it != g_solvers.end()) {
+    *out = it->second;
+    return LESB_OK;
+  }
+  std::vector<float> dx(im + 3, 1.f), dy(jm + 2, 1.f), dz(km + 2, 1.f);
+  lesb_desc d{};
+  d.im = im; d.jm = jm; d.km = km;
+  d.west_boundary = 1; d.east_boundary = 1;
+  d.dx1 = dx.data(); d.dy1 = dy.data(); d.dzn = dz.data();
+  d.dt = 1.f; d.device = device;
+  lesb_domain* h = nullptr;
+  int rc = lesb_create(&d, &h);
+  if (rc) return rc;
+  // keep at most a handful of solver contexts alive
+  if (g_solvers.size() >= 8) {
+    lesb_destroy(g_solvers.begin()->second);
+    g_solvers.erase(g_solvers.begin());
+  }
+  g_solvers[key] = h;
+  *out = h;
+  return LESB_OK;
+}
+
+int solver_prepare(int im, int jm, int km, const float* rhs, const lesb_coeffs* c, int device, lesb_domain** out) {
+  if (im < 1 || jm < 1 || km < 1) return fail(LESB_E_ARG, "grid dimensions must be >= 1");
+  if (!rhs || !c) return fail(LESB_E_ARG, "null argument");
+  lesb_domain* h = nullptr;
+  int rc = get_solver(im, jm, km, device, &h);
+  if (rc) return rc;
+  rc = lesb_set_coeffs(h, c);
+  if (rc) return rc;
+  rc = lesb_upload(h, LESB_RHS, rhs);
+  if (rc) return rc;
+  *out = h;
+  return LESB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lesb_solve_pressure(int im, int jm, int km, const float* p0, const float* rhs, const lesb_coeffs* c,
+                        float omega, int n_iter, int scheme, int halo_policy, float* p_out, double* residuals,
+                        int device) {
+  if (n_iter < 1) return fail(LESB_E_ARG, "n_iter must be >= 1");
+  if (scheme != LESB_REDBLACK && scheme != LESB_TWINNED) return fail(LESB_E_ARG, "unknown scheme");
+  if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
+  if (!p0 || !p_out) return fail(LESB_E_ARG, "null argument");
+  lesb_domain* h = nullptr;
+  int rc = solver_prepare(im, jm, km, rhs, c, device, &h);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  rc = ensure_partials(h, n_iter);
+  if (rc) return rc;
+  const size_t bytes = h->n_py * sizeof(float);
+  CK(cudaMemcpyAsync(h->p, p0, bytes, cudaMemcpyHostToDevice, h->st));
+  if (scheme == LESB_TWINNED) CK(cudaMemcpyAsync(h->pb, h->p, bytes, cudaMemcpyDeviceToDevice, h->st));
+  enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, halo_policy, h->partials, h->res_d,
+              nullptr, h->st, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(p_out, h->p, bytes, cudaMemcpyDeviceToHost, h->st));
+  if (residuals) CK(cudaMemcpyAsync(residuals, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+int lesb_redblack_iteration(int im, int jm, int km, float* p, const float* rhs, const lesb_coeffs* c, float omega,
+                            int halo_policy, double* residual, int device) {
+  return lesb_solve_pressure(im, jm, km, p, rhs, c, omega, 1, LESB_REDBLACK, halo_policy, p, residual, device);
+}
+
+int lesb_twinned_sweep(int im, int jm, int km, const float* src, float* dst, const float* rhs, const lesb_coeffs* c,
+                       float omega, double* residual, int device) {
+  if (!src || !dst) return fail(LESB_E_ARG, "null argument");
+  lesb_domain* h = nullptr;
+  int rc = solver_prepare(im, jm, km, rhs, c, device, &h);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  rc = ensure_partials(h, 1);
+  if (rc) return rc;
+  const size_t bytes = h->n_py * sizeof(float);
+  CK(cudaMemcpyAsync(h->p, src, bytes, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->pb, dst, bytes, cudaMemcpyHostToDevice, h->st));
+  const int nblk = sor_blocks_tw(h->g);
+  launch_tw_sweep(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, 0, h->partials, h->st);
+  // single-pass reduction: zero the second pass slot, reuse the 2-pass reducer
+  CK(cudaMemsetAsync(h->partials + nblk, 0, nblk * sizeof(double), h->st));
+  launch_reduce_res(h->partials, nblk, 1, h->res_d, h->st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(dst, h->pb, bytes, cudaMemcpyDeviceToHost, h->st));
+  if (residual) CK(cudaMemcpyAsync(residual, h->res_d, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// Shared device-side definitions for the B200 DPRI-LES kernels.
+//
+// Bitwise parity with the numpy reference rests on three rules (SURVEY
+// Appendix A): every float op rounds once (compiled with -fmad=false, no
+// fast-math, IEEE div/sqrt), operations are evaluated in the reference's
+// order, and boundary values are read through the closed-form halo maps of
+// SURVEY Appendix B.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lesb {
+
+// Stage bits for the non-finite flag word (les.py:401-409 order).
+enum : unsigned {
+  F_VELNW = 1u << 0, F_BONDV1 = 1u << 1, F_VELFG = 1u << 2, F_FEEDBF = 1u << 3,
+  F_LES = 1u << 4, F_ADAM = 1u << 5, F_PRESS = 1u << 6
+};
+
+// Geometry of one (slab) domain.  Device arrays are (im+3, jm+2, km+2): the
+// extra high-x plane holds the depth-2 velocity halo an x-slab needs for the
+// shifted derivative at local i = im (les.py:100-110).
+struct Geo {
+  int im, jm, km;
+  int sj;            // km + 2
+  long long si;      // (jm + 2) * (km + 2)
+  int ioff;          // global i = local i + ioff
+  int west_bc;       // local i = 0 plane is the physical west face
+  int east_bc;       // local i = im+1 plane is the physical east face
+};
+
+struct Spac {
+  const float* dx1;  // im + 3
+  const float* dy1;  // jm + 2
+  const float* dzn;  // km + 2
+};
+
+struct SorC {
+  const float* cn1;  // im*jm*km (interior, C order) or nullptr -> cn1s
+  float cn1s;
+  const float *cn2l, *cn2s, *cn3l, *cn3s, *cn4l, *cn4s;
+};
+
+__device__ __forceinline__ bool finite32(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+
+__device__ __forceinline__ long long cidx(const Geo& g, int i, int j, int k) {
+  return (long long)i * g.si + (long long)j * g.sj + k;
+}
+
+// OR the per-thread stage bits into the flag word: one atomic per warp at most.
+// All 32 lanes of every warp must call this (kernels never return early).
+__device__ __forceinline__ void flag_or(unsigned* flags, unsigned bits) {
+  unsigned any = __reduce_or_sync(0xffffffffu, bits);
+  unsigned tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  if (any && (tid & 31u) == 0) atomicOr(flags, any);
+}
+
+// Deterministic block reduction of a double (fixed shuffle tree, fixed warp order).
+template <int NWARPS>
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  int lane = (threadIdx.x + threadIdx.y * blockDim.x) & 31;
+  int wid = (threadIdx.x + threadIdx.y * blockDim.x) >> 5;
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = (lane < NWARPS) ? smem[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+}  // namespace lesb

@@ -1,0 +1,56 @@
+// Host-side launchers of the B200 DPRI-LES kernels (internal interface).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lesb_common.cuh"
+
+namespace lesb {
+
+// Called after every SOR pass / sweep and after the final halo
+// materialisation with the freshly written pressure buffer (x-slab halo
+// exchange for multi-GPU runs; unused on one GPU).
+struct ExchangeHook {
+  void (*fn)(void* ctx, float* p);
+  void* ctx;
+};
+
+// stages.cu
+void launch_velnw(const Geo& g, const Spac& s, float* u, float* v, float* w, const float* p, const float* fgh,
+                  float dt, cudaStream_t st);
+void launch_bondv1(const Geo& g, float* u, float* v, float* w, const float* inflow, cudaStream_t st);
+void launch_velnw_bondv1(const Geo& g, const Spac& s, const float* u, const float* v, const float* w,
+                         const float* p, const float* fgh, float dt, const float* inflow, float* ub, float* vb,
+                         float* wb, unsigned* flags, cudaStream_t st);
+void launch_velfg(const Geo& g, const Spac& s, const float* u, const float* v, const float* w, float* fgh,
+                  float vn, cudaStream_t st);
+void launch_feedbf(const Geo& g, float* u, float* v, float* w, float* fgh, const float* mask, float dt,
+                   cudaStream_t st);
+void launch_les(const Geo& g, const Spac& s, const float* u, const float* v, const float* w, float* fgh,
+                const float* csd2f, float csd2s, cudaStream_t st);
+void launch_strain(const Geo& g, const Spac& s, const float* u, const float* v, const float* w, float* out,
+                   cudaStream_t st);
+void launch_adam(float* fgh, float* fgh_old, long long n, cudaStream_t st);
+void launch_divergence(const Geo& g, const Spac& s, const float* u, const float* v, const float* w, float* out,
+                       float dt, int to_rhs, cudaStream_t st);
+void launch_fused_rhs(const Geo& g, const Spac& s, const float* ub, const float* vb, const float* wb,
+                      const float* mask, float* fgh, float* fgh_old, float* ua, float* va, float* wa, float* rhs,
+                      float vn, float dt, int do_les, const float* csd2f, float csd2s, unsigned* flags,
+                      cudaStream_t st);
+void launch_check_finite(const float* a, long long n, unsigned* flags, unsigned bit, cudaStream_t st);
+
+// sor.cu
+int sor_blocks_rb(const Geo& g);
+int sor_blocks_tw(const Geo& g);
+void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, float om, int nrd, int policy,
+                    double* partials, cudaStream_t st);
+void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rhs, const SorC& cf, float om,
+                     int policy, double* partials, cudaStream_t st);
+void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st);
+void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st);
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy);
+void enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
+                 int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
+                 const ExchangeHook* hook);
+
+}  // namespace lesb

@@ -1,0 +1,253 @@
+// SOR pressure solver kernels (reference: gmcf_mini/sor.py:162-309 and the
+// press halo les.py:341-355).
+//
+// Halo policies (solve_pressure's halo_fn):
+//   STORED (halo_fn=None): the halo keeps whatever p0 held; read it directly.
+//   PRESS  (les._pressure_halo): boundary values are read through the
+//          closed-form face remap of SURVEY Appendix B instead of being
+//          materialised before every colour pass:
+//            W  p[0,j,k]    -> p[1,j,k]  (the point itself)
+//            E  p[im+1,j,k] -> 0
+//            S  p[i,0,k]    -> p[i,jm,k]
+//            N  p[i,jm+1,k] -> p[i,1,k]
+//            B  p[i,j,0]    -> p[i,j,1]  (the point itself)
+//            T  p[i,j,km+1] -> 0
+//          A colour pass reads the pre-pass value of every remapped source:
+//          the W/B sources are the updated point itself (read before it is
+//          written) and, for even jm, the S/N sources have the other colour.
+//          For odd jm they share the colour, so the y halo planes are
+//          snapshotted before each pass instead (k_refresh_y) and read stored.
+//          One materialisation (k_press_halo) after the last pass reproduces
+//          the reference's final halo_fn call, including edges and corners.
+#include "lesb_common.cuh"
+#include "lesb_kernels.h"
+
+namespace lesb {
+
+constexpr int RB_BX = 32, RB_BY = 8;       // x: colour index along k, y: j
+constexpr int RB_NW = RB_BX * RB_BY / 32;
+
+template <int POL>
+__device__ __forceinline__ float sor_point(const Geo& g, const float* __restrict__ p, const float* __restrict__ rhs,
+                                           const SorC& cf, float om, long long c, int i, int j, int k, int y_stored,
+                                           float& pc_out) {
+  const float pc = p[c];
+  float pE, pW, pN, pS, pT, pB;
+  if (POL == 1) {
+    pE = (i == g.im && g.east_bc) ? 0.0f : p[c + g.si];
+    pW = (i == 1 && g.west_bc) ? pc : p[c - g.si];
+    pN = (j == g.jm && !y_stored) ? p[c - (long long)(g.jm - 1) * g.sj] : p[c + g.sj];
+    pS = (j == 1 && !y_stored) ? p[c + (long long)(g.jm - 1) * g.sj] : p[c - g.sj];
+    pT = (k == g.km) ? 0.0f : p[c + 1];
+    pB = (k == 1) ? pc : p[c - 1];
+  } else {
+    pE = p[c + g.si];
+    pW = p[c - g.si];
+    pN = p[c + g.sj];
+    pS = p[c - g.sj];
+    pT = p[c + 1];
+    pB = p[c - 1];
+  }
+  // sor.py:164-171: E, W, N, S, T, B summed left to right
+  float nb = cf.cn2l[i - 1] * pE;
+  nb = nb + cf.cn2s[i - 1] * pW;
+  nb = nb + cf.cn3l[j - 1] * pN;
+  nb = nb + cf.cn3s[j - 1] * pS;
+  nb = nb + cf.cn4l[k - 1] * pT;
+  nb = nb + cf.cn4s[k - 1] * pB;
+  const float cn1 = cf.cn1 ? cf.cn1[((long long)(i - 1) * g.jm + (j - 1)) * g.km + (k - 1)] : cf.cn1s;
+  pc_out = pc;
+  // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+  return om * (cn1 * (nb - rhs[c]) - pc);
+}
+
+// One red-black colour pass, in place (sor.py:194-200).  Thread x enumerates
+// the colour's cells along k: k = 1 + ((i0 + j0 + nrd) & 1) + 2 t.
+template <int POL>
+__global__ void __launch_bounds__(RB_BX* RB_BY) k_sor_rb(Geo g, float* __restrict__ p, const float* __restrict__ rhs,
+                                                         SorC cf, float om, int nrd, int y_stored,
+                                                         double* __restrict__ partials) {
+  __shared__ double red[RB_NW];
+  const int t = blockIdx.x * RB_BX + threadIdx.x;
+  const int j = blockIdx.y * RB_BY + threadIdx.y + 1;
+  const int i = blockIdx.z + 1;
+  double acc = 0.0;
+  if (j <= g.jm) {
+    const int ig0 = i + g.ioff - 1;
+    const int k = 1 + ((ig0 + (j - 1) + nrd) & 1) + 2 * t;
+    if (k <= g.km) {
+      const long long c = cidx(g, i, j, k);
+      float pc;
+      const float rel = sor_point<POL>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
+      p[c] = pc + rel;
+      acc = (double)rel * (double)rel;
+    }
+  }
+  const double s = block_sum<RB_NW>(acc, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    partials[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+}
+
+// One twinned (Jacobi) sweep: read src everywhere, write the interior of dst
+// (sor.py:206-246).
+constexpr int TW_BX = 32, TW_BY = 8, TW_NW = TW_BX * TW_BY / 32;
+
+template <int POL>
+__global__ void __launch_bounds__(TW_BX* TW_BY) k_sor_tw(Geo g, const float* __restrict__ src,
+                                                         float* __restrict__ dst, const float* __restrict__ rhs,
+                                                         SorC cf, float om, double* __restrict__ partials) {
+  __shared__ double red[TW_NW];
+  const int k = blockIdx.x * TW_BX + threadIdx.x + 1;
+  const int j = blockIdx.y * TW_BY + threadIdx.y + 1;
+  const int i = blockIdx.z + 1;
+  double acc = 0.0;
+  if (j <= g.jm && k <= g.km) {
+    const long long c = cidx(g, i, j, k);
+    float pc;
+    const float rel = sor_point<POL>(g, src, rhs, cf, om, c, i, j, k, 0, pc);
+    dst[c] = pc + rel;
+    acc = (double)rel * (double)rel;
+  }
+  const double s = block_sum<TW_NW>(acc, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    partials[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+}
+
+// Snapshot of the y halo planes used by the stencils (odd jm, PRESS policy).
+__global__ void k_refresh_y(Geo g, float* __restrict__ p) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int i = blockIdx.y + 1;
+  if (k > g.km) return;
+  p[cidx(g, i, 0, k)] = p[cidx(g, i, g.jm, k)];
+  p[cidx(g, i, g.jm + 1, k)] = p[cidx(g, i, 1, k)];
+}
+
+// Final halo_fn(p) of the press policy in closed form: resolve k (0 -> 1,
+// km+1 -> 0), then j (periodic), then i (0 -> 1, im+1 -> 0).  Optionally
+// checks every cell of p for finiteness (press stage, les.py:413-415).
+__global__ void k_press_halo(Geo g, float* __restrict__ p, unsigned* flags) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int i = blockIdx.z;
+  unsigned bits = 0;
+  if (k <= g.km + 1 && j <= g.jm + 1) {
+    const long long c = cidx(g, i, j, k);
+    const bool halo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1 || k == 0 || k == g.km + 1;
+    const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+    float val;
+    if (halo && !foreign) {
+      if (k == g.km + 1 || i == g.im + 1) {
+        val = 0.0f;
+      } else {
+        const int kk = k == 0 ? 1 : k;
+        const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
+        const int ii = i == 0 ? 1 : i;
+        val = p[cidx(g, ii, jj, kk)];
+      }
+      p[c] = val;
+    } else {
+      val = p[c];
+    }
+    if (flags && !finite32(val)) bits = F_PRESS;
+  }
+  if (flags) flag_or(flags, bits);
+}
+
+// residuals[it] = (sum of pass-0 partials) + (sum of pass-1 partials), each
+// summed by one fixed-order tree (deterministic; numpy's pairwise order is
+// matched only to rtol ~1e-15).
+__global__ void k_reduce_res(const double* __restrict__ partials, int nblk, double* __restrict__ out) {
+  __shared__ double red[8];
+  const int it = blockIdx.x;
+  double tot = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* q = partials + ((long long)it * 2 + pass) * nblk;
+    double a = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) a += q[b];
+    a = block_sum<8>(a, red);
+    __syncthreads();
+    if (threadIdx.x == 0) tot += a;
+  }
+  if (threadIdx.x == 0) out[it] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int sor_blocks_rb(const Geo& g) {
+  const int kh = (g.km + 1) / 2;
+  return ((kh + RB_BX - 1) / RB_BX) * ((g.jm + RB_BY - 1) / RB_BY) * g.im;
+}
+int sor_blocks_tw(const Geo& g) {
+  return ((g.km + TW_BX - 1) / TW_BX) * ((g.jm + TW_BY - 1) / TW_BY) * g.im;
+}
+
+void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, float om, int nrd, int policy,
+                    double* partials, cudaStream_t st) {
+  const int kh = (g.km + 1) / 2;
+  dim3 grid((kh + RB_BX - 1) / RB_BX, (g.jm + RB_BY - 1) / RB_BY, g.im);
+  dim3 block(RB_BX, RB_BY);
+  const int y_stored = (policy == 1 && (g.jm & 1)) ? 1 : 0;
+  if (y_stored) {
+    dim3 gy((g.km + 127) / 128, g.im);
+    k_refresh_y<<<gy, 128, 0, st>>>(g, p);
+  }
+  if (policy == 1) k_sor_rb<1><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, y_stored, partials);
+  else k_sor_rb<0><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, 0, partials);
+}
+
+void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rhs, const SorC& cf, float om,
+                     int policy, double* partials, cudaStream_t st) {
+  dim3 grid((g.km + TW_BX - 1) / TW_BX, (g.jm + TW_BY - 1) / TW_BY, g.im);
+  dim3 block(TW_BX, TW_BY);
+  if (policy == 1) k_sor_tw<1><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+  else k_sor_tw<0><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+}
+
+void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st) {
+  int nk = g.km + 2;
+  int bx = ((nk + 31) / 32) * 32;
+  if (bx > 128) bx = 128;
+  int by = 256 / bx;
+  dim3 grid((nk + bx - 1) / bx, (g.jm + 2 + by - 1) / by, g.im + 2);
+  k_press_halo<<<grid, dim3(bx, by), 0, st>>>(g, p, flags);
+}
+
+void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st) {
+  k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
+}
+
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy) {
+  int per_iter = 2;
+  if (scheme == 0 && policy == 1 && (g.jm & 1)) per_iter = 4;
+  return per_iter * n_iter + (policy == 1 ? 1 : 0) + 1;
+}
+
+// Enqueue a full solve on p (in place).  TWINNED needs pb initialised to a
+// copy of p by the caller (make_twinned, sor.py:145-150).
+void enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
+                 int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
+                 const ExchangeHook* hook) {
+  const int nblk = scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g);
+  for (int it = 0; it < n_iter; ++it) {
+    for (int nrd = 0; nrd < 2; ++nrd) {
+      double* part = partials + ((long long)it * 2 + nrd) * nblk;
+      if (scheme == 0) {
+        launch_rb_pass(g, p, rhs, cf, om, nrd, policy, part, st);
+        if (hook && hook->fn) hook->fn(hook->ctx, p);
+      } else {
+        const float* s = nrd == 0 ? p : pb;
+        float* d = nrd == 0 ? pb : p;
+        launch_tw_sweep(g, s, d, rhs, cf, om, policy, part, st);
+        if (hook && hook->fn) hook->fn(hook->ctx, d);
+      }
+    }
+  }
+  if (policy == 1) {
+    launch_press_halo(g, p, flags, st);
+    if (hook && hook->fn) hook->fn(hook->ctx, p);
+  }
+  launch_reduce_res(partials, nblk, n_iter, res_dev, st);
+}
+
+}  // namespace lesb

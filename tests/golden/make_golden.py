@@ -177,13 +177,34 @@ def large(meta: dict):
     meta["config2"] = rec
 
 
+def blowups(meta: dict):
+    """Blow-up step and stage at full size (probes P4/P10):
+    config 2 with buildings and the building-free 150x150x90 flow."""
+    t0 = time.time()
+    for name, st in (("config2", gi.config2_state()), ("free150", gi.zero_state(150, 150, 90))):
+        fs = to_flow(st)
+        inflow = WindProfile(*gi.default_inflow(90))
+        rec = {}
+        for s in range(1, 80):
+            try:
+                les.step(fs, inflow)
+            except NumericsError as e:
+                rec = {"step": s, "stage": e.stage}
+                break
+        meta[f"blowup_{name}"] = rec
+        print(name, rec, f"{time.time()-t0:.0f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
+    ap.add_argument("--blowup", action="store_true")
     args = ap.parse_args()
     meta_path = os.path.join(HERE, "golden_meta.json")
     meta = json.load(open(meta_path)) if os.path.exists(meta_path) else {}
-    if args.large:
+    if args.blowup:
+        blowups(meta)
+    elif args.large:
         large(meta)
     else:
         out: dict = {}

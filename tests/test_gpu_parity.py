@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors of
+the unmodified reference and against the CPU oracle.  Bitwise for every
+float32 field; float64 residual sums within rtol 1e-12 (summation order).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import golden_inputs as gi
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = np.load(os.path.join(HERE, "golden", "small.npz"))
+META = json.load(open(os.path.join(HERE, "golden", "golden_meta.json")))
+FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p")
+RTOL_RES = 1e-12
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1504_02264_b200 as pkg
+
+    return pkg
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def dstate(P, st):
+    g = P.Grid(st["im"], st["jm"], st["km"], st["dx1"], st["dy1"], st["dzn"])
+    fs = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    for n in FIELDS + ("mask",):
+        getattr(fs, n)[...] = st[n]
+    return fs
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def assert_state(fs, prefix):
+    for n in FIELDS:
+        got = getattr(fs, n)
+        exp = GOLD[prefix + n]
+        if not bits_equal(got, exp):
+            diff = np.argwhere(got.view(np.uint32) != exp.view(np.uint32))
+            raise AssertionError(f"{prefix}{n}: {len(diff)} cells differ, first {diff[:5].tolist()} "
+                                 f"got {got[tuple(diff[0])]} exp {exp[tuple(diff[0])]}")
+
+
+@pytest.mark.parametrize("tag,dims,uniform", gi.STAGE_CASES)
+def test_stages_bitwise(P, tag, dims, uniform):
+    st = gi.random_state(*dims, seed=gi.seed_of(tag), uniform=uniform)
+    inflow = P.WindProfile(*gi.random_inflow(dims[2], seed=gi.seed_of(tag) + 1))
+    calls = {
+        "velnw": P.les.velnw,
+        "bondv1": lambda fs: P.les.bondv1(fs, inflow),
+        "velfg": P.les.velfg_merged,
+        "feedbf": P.les.feedbf,
+        "les": P.les.les_viscosity,
+        "adam": P.les.adam,
+    }
+    if uniform:
+        calls["press"] = lambda fs: P.les.press(fs, n_iter=7)
+        calls["press_tw"] = lambda fs: P.les.press(fs, n_iter=7, scheme=P.Scheme.TWINNED)
+    for name, fn in calls.items():
+        fs = dstate(P, st)
+        res = fn(fs)
+        assert_state(fs, f"{tag}/{name}/")
+        if name.startswith("press"):
+            np.testing.assert_allclose(res, GOLD[f"{tag}/{name}/res"], rtol=RTOL_RES, atol=0)
+    fs = dstate(P, st)
+    assert bits_equal(P.les.divergence(fs), GOLD[f"{tag}/divergence"])
+    assert bits_equal(P.les.strain_magnitude(fs), GOLD[f"{tag}/strain"])
+
+
+@pytest.mark.parametrize("tag,dims,h", gi.SOR_CASES)
+def test_sor_bitwise(P, tag, dims, h):
+    p0, rhs = gi.sor_problem(*dims, seed=gi.seed_of(tag))
+    grid = P.Grid.uniform(*dims, h)
+    c = P.sor.build_uniform_coeffs(grid)
+    halo = P.les._pressure_halo(grid)
+    for scheme, om in ((P.Scheme.REDBLACK, 1.7), (P.Scheme.TWINNED, 1.0)):
+        for pol, fn in (("stored", None), ("press", halo)):
+            p0c = p0.copy()
+            p, res = P.sor.solve_pressure(p0c, rhs, c, om, 9, scheme, 1, halo_fn=fn)
+            assert bits_equal(p0c, p0), "p0 must not be modified"
+            assert bits_equal(p, GOLD[f"{tag}/{scheme.value}/{pol}/p"]), (scheme, pol)
+            np.testing.assert_allclose(res, GOLD[f"{tag}/{scheme.value}/{pol}/res"], rtol=RTOL_RES, atol=0)
+    p = p0.copy()
+    r = P.sor.redblack_iteration(p, rhs, c, 1.7, halo)
+    assert bits_equal(p, GOLD[f"{tag}/rbiter/p"])
+    np.testing.assert_allclose(r, GOLD[f"{tag}/rbiter/res"][0], rtol=RTOL_RES)
+    tp = GOLD[f"{tag}/twsweep/in"].copy()
+    r = P.sor.twinned_sweep(tp, rhs, c, 1.0, 1)
+    assert bits_equal(tp, GOLD[f"{tag}/twsweep/out"])
+    np.testing.assert_allclose(r, GOLD[f"{tag}/twsweep/res"][0], rtol=RTOL_RES)
+
+
+@pytest.mark.parametrize("tag,dims,n_steps", gi.STEP_CASES)
+def test_step_bitwise(P, tag, dims, n_steps):
+    fs = dstate(P, gi.step_state(tag, *dims))
+    inflow = P.WindProfile(*gi.step_inflow(tag, dims[2]))
+    scheme = P.Scheme(gi.STEP_SCHEME[tag])
+    for s in range(1, n_steps + 1):
+        P.les.step(fs, inflow, n_iter=gi.STEP_NITER[tag], scheme=scheme)
+        if s in (1, n_steps):
+            assert_state(fs, f"{tag}/step{s}/")
+
+
+def test_config1_anchors_and_blowup(P):
+    """32x32x16, one building, RB50: reference hashes at steps 1 and 10 and
+    the NumericsError at step 17 in velfg."""
+    meta = META["config1"]
+    fs = dstate(P, gi.config1_state())
+    inflow = P.WindProfile(*gi.default_inflow(16))
+    step = 0
+    with pytest.raises(P.NumericsError) as err:
+        while step < 40:
+            P.les.step(fs, inflow)
+            step += 1
+            if step in (1, 10):
+                for n in FIELDS:
+                    assert sha(getattr(fs, n)) == meta[f"step{step}"][n], (step, n)
+    assert step + 1 == meta["blowup"]["step"]
+    assert err.value.stage == meta["blowup"]["stage"]
+
+
+def test_run_steps_matches_step_loop(P):
+    """The batched API (one host sync) gives the same state and reports the
+    same failing step and stage as the step-by-step loop."""
+    inflow = P.WindProfile(*gi.default_inflow(16))
+    a = dstate(P, gi.config1_state())
+    assert P.les.run_steps(a, inflow, 10) == 10
+    for n in FIELDS:
+        assert sha(getattr(a, n)) == META["config1"]["step10"][n], n
+    b = dstate(P, gi.config1_state())
+    with pytest.raises(P.NumericsError) as err:
+        P.les.run_steps(b, inflow, 30)
+    assert err.value.step + 1 == META["config1"]["blowup"]["step"]
+    assert err.value.stage == "velfg"
+
+
+def test_blowup_stage_velnw(P):
+    """test_les.py:307-312: an inf in u is reported by the velnw stage."""
+    fs = P.FlowState.create(P.Grid.uniform(8, 8, 8, 1.0), dt=0.5)
+    fs.u[1, 1, 1] = np.inf
+    z = np.zeros(8, np.float32)
+    with pytest.raises(P.NumericsError) as err:
+        P.les.step(fs, P.WindProfile(z, z, z), n_iter=2)
+    assert err.value.stage == "velnw"
+
+
+def test_quiescent_fixed_point(P):
+    """test_les.py:280-284"""
+    fs = P.FlowState.create(P.Grid.uniform(8, 8, 8, 1.0), dt=0.5)
+    z = np.zeros(8, np.float32)
+    P.les.step(fs, P.WindProfile(z, z, z), n_iter=5)
+    for n in FIELDS:
+        assert np.all(getattr(fs, n) == 0.0), n
+
+
+def test_step_against_oracle_odd_shapes(P):
+    """Extra shapes the golden set does not cover (odd jm with RB, jm = 1,
+    km = 1), GPU vs the CPU oracle for 4 steps."""
+    from oracle import les_oracle as O
+
+    for (im, jm, km), scheme in (((7, 5, 3), "redblack"), ((5, 1, 4), "redblack"), ((6, 4, 1), "twinned"),
+                                 ((3, 3, 3), "twinned")):
+        st = gi.random_state(im, jm, km, seed=im * 100 + jm * 10 + km, vel_scale=0.2)
+        inflow = gi.random_inflow(km, seed=7)
+        fs = dstate(P, st)
+        o = O.OState.zeros(im, jm, km)
+        for n in FIELDS + ("mask", "dx1", "dy1", "dzn"):
+            getattr(o, n)[...] = st[n]
+        for s in range(4):
+            P.les.step(fs, P.WindProfile(*inflow), n_iter=11, scheme=P.Scheme(scheme))
+            O.step(o, *inflow, n_iter=11, scheme=scheme)
+            for n in FIELDS:
+                assert bits_equal(getattr(fs, n), getattr(o, n)), ((im, jm, km), scheme, s, n)
+
+
+def test_press_150_anchors(P):
+    """press-only 150x150x90, h=1, rng(0) rhs, 50 iterations."""
+    rec = META.get("press150")
+    if rec is None:
+        pytest.skip("large golden vectors not generated")
+    im, jm, km = 150, 150, 90
+    rng = np.random.default_rng(0)
+    rhs = P.sor.make_field(im, jm, km)
+    rhs[1:-1, 1:-1, 1:-1] = rng.uniform(-1, 1, size=(im, jm, km)).astype(np.float32)
+    p0 = P.sor.make_field(im, jm, km)
+    grid = P.Grid.uniform(im, jm, km, 1.0)
+    c = P.sor.build_uniform_coeffs(grid)
+    for name, scheme, om, fn in (("rb_zero", P.Scheme.REDBLACK, 1.7, None),
+                                 ("rb_press", P.Scheme.REDBLACK, 1.7, P.les._pressure_halo(grid)),
+                                 ("tw_zero", P.Scheme.TWINNED, 1.0, None)):
+        p, res = P.sor.solve_pressure(p0, rhs, c, om, 50, scheme, 1, halo_fn=fn)
+        assert sha(p) == rec[name]["sha_p"], name
+        np.testing.assert_allclose(res, rec[name]["res"], rtol=RTOL_RES, atol=0)
+
+
+def test_config2_150_anchors(P):
+    """Config 2: 150x150x90 with the 3x3 building array, hashes of all six
+    fields after steps 1 and 10 (the reference's own values)."""
+    rec = META.get("config2")
+    if rec is None:
+        pytest.skip("large golden vectors not generated")
+    fs = dstate(P, gi.config2_state())
+    inflow = P.WindProfile(*gi.default_inflow(90))
+    for s in range(1, 11):
+        P.les.step(fs, inflow)
+        if s in (1, 10):
+            for n in FIELDS:
+                assert sha(getattr(fs, n)) == rec[f"step{s}"][n], (s, n)
+
+
+@pytest.mark.parametrize("name", ["config2", "free150"])
+def test_blowup_150(P, name):
+    """Blow-up step and stage at 150x150x90 equal the reference's."""
+    rec = META.get(f"blowup_{name}")
+    if not rec:
+        pytest.skip("blow-up golden not generated")
+    st = gi.config2_state() if name == "config2" else gi.zero_state(150, 150, 90)
+    fs = dstate(P, st)
+    inflow = P.WindProfile(*gi.default_inflow(90))
+    with pytest.raises(P.NumericsError) as err:
+        P.les.run_steps(fs, inflow, 80)
+    assert err.value.step + 1 == rec["step"]
+    assert err.value.stage == rec["stage"]
+
+
+def test_determinism(P):
+    """Two identical runs give identical fields and residuals (acceptance 8)."""
+    outs = []
+    for _ in range(2):
+        fs = dstate(P, gi.config1_state())
+        inflow = P.WindProfile(*gi.default_inflow(16))
+        for _s in range(3):
+            P.les.step(fs, inflow)
+        res = P.les.press(fs, n_iter=5)
+        outs.append((fs.sync(), res))
+    for n in FIELDS:
+        assert bits_equal(getattr(outs[0][0], n), getattr(outs[1][0], n))
+    assert np.array_equal(outs[0][1], outs[1][1])
