@@ -1,0 +1,372 @@
+"""Benchmark: DPRI-LES time steps/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): 150x150x90 grid,
+h = 2, dt = 0.5, vn = 0.8, cs = 0.14, the 3x3 synthetic building array,
+WRF-style log-law inflow, red-black SOR with 50 iterations (les.step
+defaults).  Synthetic data.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Arms
+  (default)    the CUDA path.  `value` = steps/s with the state resident in
+               HBM, each step one CUDA-graph replay timed with CUDA events on
+               the domain stream, L2 flushed (256 MB write) before every
+               timed step.  The reference dynamics blow up at step 19 with
+               buildings, so the state is re-initialised
+               (untimed device copy) every 8 steps; kernel cost is
+               data-independent.
+               `e2e` = the same steps through the public Python API
+               (les.step on a FlowState), timed on the host clock per
+               8-step window that uploads the initial state from pinned host
+               memory, runs 8 steps (inflow H2D, stage flags + residual
+               history D2H per step) and downloads the six fields.
+  reference    the reference algorithm on the host CPU: the numpy port in
+               oracle/ (the reference is pure Python/numpy; single-threaded
+               RB path, 1 core), a bounded sample of full-size steps.
+
+Multi-GPU (torchrun, N > 1): replicas -- each rank runs the 150x150x90
+workload on its own GPU ("scaling": "weak"); value sums steps over ranks
+divided by the max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "LES time steps/sec and MLUPS at 1/2/4/8 B200; % of HBM-bandwidth roofline"
+IM, JM, KM = 150, 150, 90
+N_ITER = 50
+REINIT = 8
+B_STEP = 216 + 16 * N_ITER      # algorithmic bytes / interior cell / step
+B_PASS_SCALAR_CN1 = 6           # one RB colour pass, cn1 scalar: (4 p r/w + 4 rhs) / 2 ... see DESIGN.md
+WORKLOAD = "config2: 150x150x90, h=2, dt=0.5, 3x3 buildings, log-law inflow, RB SOR 50 iters"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm and CPU baseline (oracle port of the reference)
+# ---------------------------------------------------------------------------
+def cpu_sample(max_steps: int, budget_s: float):
+    """Time full-size oracle steps (the reference's numpy algorithm) on host
+    cores: returns (steps/s, steps timed, seconds)."""
+    import golden_inputs as gi
+    from oracle import les_oracle as O
+
+    st = gi.config2_state()
+    o = O.OState.zeros(IM, JM, KM)
+    for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask", "dx1", "dy1", "dzn"):
+        getattr(o, n)[...] = st[n]
+    inflow = gi.default_inflow(KM)
+    done = 0
+    t0 = time.perf_counter()
+    while done < max_steps:
+        O.step(o, *inflow, n_iter=N_ITER)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample(1, 0)
+    rate, n, secs = cpu_sample(max(1, args.steps), 90.0)
+    cores = 1
+    sample = f"{n} full 150x150x90 RB50 steps of the numpy port (oracle/les_oracle.py), 1 thread"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1000.0 / rate, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack"},
+        "mlups": rate * IM * JM * KM / 1e6,
+        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CUDA arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    import golden_inputs as gi
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200 import _native as N
+
+    P.runtime.set_device(local)
+    lib = N.load()
+    st0 = gi.config2_state()
+    grid = P.Grid(IM, JM, KM, st0["dx1"], st0["dy1"], st0["dzn"])
+    inflow = P.WindProfile(*gi.default_inflow(KM))
+
+    def make_state():
+        fs = P.FlowState.create(grid, dt=0.5, vn=0.8, cs=0.14)
+        fs.mask[...] = st0["mask"]
+        return fs
+
+    pristine = make_state()
+    hp = pristine.handle()
+    pristine._ensure_coeffs(hp)
+    work = make_state()
+    hw = work.handle()
+    work._ensure_coeffs(hw)
+    arrs = [N.f32c(getattr(inflow, c)) for c in ("u", "v", "w")]
+    N.check(lib.lesb_set_inflow(hw.h, *[N.fptr(a) for a in arrs]), "set_inflow")
+    N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
+    stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0) + 1  # + async bookkeeping kernel
+    sor_path = {1: "streaming colour passes", 2: "shared-memory-resident persistent kernel"}[
+        lib.lesb_sor_path_in_use(hw.h, 0)]
+
+    def reinit():
+        N.check(lib.lesb_copy_state(hw.h, hp.h), "copy_state")
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    phase_ms = np.zeros(4)
+    since = 0
+    reinit()
+    # warm-up
+    for _ in range(args.warmup):
+        if since == REINIT:
+            reinit()
+            since = 0
+        N.check(lib.lesb_step_async(hw.h, N_ITER, 0, 1.7), "step")
+        since += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            if since == REINIT:
+                reinit()
+                since = 0
+            with torch.cuda.stream(stream):
+                flush.fill_(float(s))
+                ev[s][0].record(stream)
+            N.check(lib.lesb_step_async(hw.h, N_ITER, 0, 1.7), "step")
+            with torch.cuda.stream(stream):
+                ev[s][1].record(stream)
+            since += 1
+            ph = np.zeros(4, np.float32)
+            N.check(lib.lesb_last_step_times(hw.h, N.fptr(ph)), "times")
+            phase_ms += ph
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    done = N.C.c_int(0)
+    fstep = N.C.c_int(-1)
+    fstage = N.C.c_int(-1)
+    N.check(lib.lesb_poll_failure(hw.h, N.C.byref(done), N.C.byref(fstep), N.C.byref(fstage)), "poll")
+    if fstep.value >= 0:
+        raise RuntimeError(f"benchmark state went non-finite at step {fstep.value} ({fstage.value})")
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    ms_per_step = dev_ms / args.steps
+    value = world * args.steps / (dev_ms / 1000.0)  # replicas: steps over all ranks / max time
+    n_int = IM * JM * KM
+    hbm, peak_kind = peaks()
+    phase_ms /= args.steps
+    sor_pass_ms = phase_ms[2] / (2 * N_ITER)
+    b_pass = 6 * n_int  # see DESIGN.md "algorithmic bytes": RB pass, scalar cn1
+    achieved = b_pass / (sor_pass_ms * 1e-3) / 1e9
+    step_gbs = B_STEP * n_int / (ms_per_step * 1e-3) / 1e9
+
+    # ---- e2e through the public API ----
+    e2e = (e2e_run(P, N, gi, torch, grid, st0, inflow, args) if not args.no_e2e
+           else {"value": None, "seconds": 0.0, "h2d": 0, "d2h": 0})
+    if world > 1:
+        t = torch.tensor([e2e["seconds"]], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["seconds"] = float(t.item())
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rate, n, secs = cpu_sample(3, 20.0)
+        cpu = {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
+               "sample": f"{n} full 150x150x90 RB50 steps of the numpy port in {secs:.1f}s, 1 thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack",
+                       "l2": "flushed before every timed step (256 MB device write, untimed)",
+                       "reinit_every_steps": REINIT, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "timing": "CUDA events on the domain stream around each CUDA-graph step replay",
+                       "sor_kernel": sor_path},
+            "mlups": value * n_int / 1e6,
+            "step_roofline": {"bytes_per_cell": B_STEP, "achieved_gbs": step_gbs, "peak_gbs": hbm,
+                              "frac": step_gbs / hbm, "peak_kind": peak_kind},
+            "phase_ms": {"velnw_bondv1": phase_ms[0], "velfg_feedbf_les_adam_rhs": phase_ms[1],
+                         "sor_passes": phase_ms[2], "halo_and_residuals": phase_ms[3]},
+            "roofline": {"kernel": "k_sor_rb (one red-black colour pass)", "bound": "hbm",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": b_pass, "launch_ms": sor_pass_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e["value"], "unit": "steps/s", "h2d_bytes_per_step": e2e["h2d"],
+                    "d2h_bytes_per_step": e2e["d2h"]},
+            "gpu_launches": kps * args.steps,
+            "clocks": clk.summary(),
+            "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(P, N, gi, torch, grid, st0, inflow, args):
+    """Public-API steps with host buffers, timed on the host clock."""
+    names = ("u", "v", "w", "fgh", "fgh_old", "p", "mask")
+    work = {n: torch.empty(st0[n].shape, dtype=torch.float32, pin_memory=True).numpy() for n in names}
+    fs = P.FlowState.create(grid, dt=0.5, vn=0.8, cs=0.14)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def window():
+        for n in names:
+            setattr(fs, n, work[n])            # host arrays -> uploaded before the first step
+        for _s in range(REINIT):
+            P.les.step(fs, inflow)             # inflow H2D, stage flags + residuals D2H
+        for n in names[:6]:
+            getattr(fs, n)                     # device -> host (into work[n])
+
+    for n in names:
+        work[n][...] = st0[n]
+    window()                                   # warm-up: graph capture
+    n_windows = max(1, args.steps // REINIT)
+    secs = 0.0
+    for _ in range(n_windows):
+        for n in names:
+            work[n][...] = st0[n]
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        window()
+        secs += time.perf_counter() - t0
+    h2d = sum(work[n].nbytes for n in names) / REINIT + 3 * KM * 4
+    d2h = sum(work[n].nbytes for n in names[:6]) / REINIT + 4 + 8 * N_ITER
+    return {"value": n_windows * REINIT / secs, "seconds": secs, "h2d": int(h2d), "d2h": int(d2h)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e measurement (profiling runs)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "cuda":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

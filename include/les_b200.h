@@ -137,8 +137,26 @@ int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profil
 int lesb_set_inflow(lesb_handle h, const float* in_u, const float* in_v, const float* in_w);
 int lesb_step_async(lesb_handle h, int n_iter, int scheme, float omega);
 int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_stage);
-/* Number of kernel launches one step enqueues (evidence for gpu_launches). */
+/* Number of kernel launches one step enqueues (evidence for gpu_launches;
+ * the asynchronous variant adds one bookkeeping kernel). */
 int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme);
+/* Device-to-device copy of the seven state fields between two domains of
+ * the same shape on the same device (benchmark re-initialisation). */
+int lesb_copy_state(lesb_handle dst, lesb_handle src);
+/* Capture CUDA events between the step phases; lesb_last_step_times then
+ * returns, for the last replayed step, ms of [velnw+bondv1, fused
+ * velfg..rhs, SOR passes, halo + residual reduction]. */
+int lesb_set_timing(lesb_handle h, int on);
+/* Red-black solver implementation: 0 auto (shared-memory-resident persistent
+ * kernel when the grid fits the SMs' shared memory and cn1 is constant,
+ * else streaming colour passes), 1 streaming only, 2 resident when possible.
+ * Results are bitwise identical either way. */
+int lesb_set_sor_path(lesb_handle h, int path);
+int lesb_sor_path_in_use(lesb_handle h, int scheme);  /* 1 streaming, 2 resident */
+/* Default for domains created afterwards and for the host-buffer solver
+ * entry points (initially $LESB_SOR_PATH or 0). */
+int lesb_set_default_sor_path(int path);
+int lesb_last_step_times(lesb_handle h, float* ms4);
 
 /* ---- SOR solver on host buffers (sor.py:181-309) ---- */
 /* solve_pressure(p0, rhs, c, omega, n_iter, scheme, workers, halo_fn):

@@ -72,6 +72,12 @@ _SIGS = {
     "lesb_step_async": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_float]),
     "lesb_poll_failure": (C.c_int, [C.c_void_p, IP, IP, IP]),
     "lesb_kernels_per_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "lesb_copy_state": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "lesb_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "lesb_set_sor_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "lesb_sor_path_in_use": (C.c_int, [C.c_void_p, C.c_int]),
+    "lesb_set_default_sor_path": (C.c_int, [C.c_int]),
+    "lesb_last_step_times": (C.c_int, [C.c_void_p, FP]),
     "lesb_solve_pressure": (C.c_int, [C.c_int, C.c_int, C.c_int, FP, FP, C.POINTER(lesb_coeffs),
                                       C.c_float, C.c_int, C.c_int, C.c_int, FP, DP, C.c_int]),
     "lesb_redblack_iteration": (C.c_int, [C.c_int, C.c_int, C.c_int, FP, FP, C.POINTER(lesb_coeffs),

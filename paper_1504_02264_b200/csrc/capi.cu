@@ -6,6 +6,7 @@
 // coefficients.  One time step is captured once into a CUDA graph per
 // (n_iter, scheme, omega) and replayed.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -22,6 +23,24 @@ using namespace lesb;
 namespace {
 
 thread_local std::string g_err;
+
+std::mutex& g_solver_mu_fwd() {
+  static std::mutex m;
+  return m;
+}
+std::map<std::tuple<int, int, int, int>, lesb_domain*>& solver_map() {
+  static std::map<std::tuple<int, int, int, int>, lesb_domain*> m;
+  return m;
+}
+
+int default_sor_path() {
+  static int v = [] {
+    const char* e = std::getenv("LESB_SOR_PATH");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+int g_default_sor_path = -1;
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -42,6 +61,7 @@ struct StepBook {
   unsigned steps;       // steps enqueued and completed on the device
   int fail_step;        // -1 while no step failed
   unsigned fail_flags;  // stage bits of the first failing step
+  unsigned err;         // device-side solver error (neighbour wait timed out)
 };
 
 __global__ void k_step_tail(StepBook* b) {
@@ -86,6 +106,11 @@ struct lesb_domain {
   int res_cap = 0;
   float* scratch = nullptr;  // im*jm*km
   std::map<std::tuple<int, int, int, unsigned>, cudaGraphExec_t> graphs;
+  bool timing = false;
+  int sor_path = 0;  // 0 auto, 1 streaming kernels, 2 shared-memory-resident solver
+  float* xbuf = nullptr;
+  unsigned* rflags = nullptr;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool known_finite = false;
   long long n_alloc = 0;  // (im+3)*si
   long long n_py = 0;     // (im+2)*si : the Python-visible array
@@ -93,18 +118,24 @@ struct lesb_domain {
 
   Spac spac() const { return Spac{dx1, dy1, dzn}; }
   SorC sorc() const { return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5]}; }
+  ResidentBufs rbufs() const { return ResidentBufs{sor_path != 1 && xbuf != nullptr, device, xbuf, rflags, &book_d->err}; }
   long long n_int() const { return (long long)g.im * g.jm * g.km; }
 };
 
 namespace {
 
 int ensure_partials(lesb_domain* h, int n_iter) {
-  long long need = (long long)n_iter * 2 * std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g));
+  long long need = (long long)n_iter * 2 *
+                   std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_ntiles(h->g, h->device));
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
     h->partials = nullptr;
     CK(cudaMalloc(&h->partials, need * sizeof(double)));
     h->partials_cap = need;
+  }
+  if (h->sor_path != 1 && !h->xbuf && resident_supported(h->g, h->sorc(), h->device)) {
+    CK(cudaMalloc(&h->xbuf, resident_xbuf_floats(h->g, h->device) * sizeof(float)));
+    CK(cudaMalloc(&h->rflags, resident_ntiles(h->g, h->device) * sizeof(unsigned)));
   }
   if (n_iter > h->res_cap) {
     if (h->res_d) cudaFree(h->res_d);
@@ -140,26 +171,42 @@ float* field_ptr(lesb_domain* h, int f) {
 long long field_count(lesb_domain* h, int f) { return (f == LESB_FGH || f == LESB_FGH_OLD) ? 3 * h->n_py : h->n_py; }
 
 // Enqueue the press stage on the stream: rhs = div(u)/dt, SOR, final halo.
-void enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, bool rhs_from_state, unsigned* flags) {
+cudaError_t enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, bool rhs_from_state,
+                          unsigned* flags) {
   if (rhs_from_state) launch_divergence(h->g, h->spac(), h->u, h->v, h->w, h->rhs, h->dt, 1, h->st);
-  enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d, flags, h->st,
-              nullptr);
+  ResidentBufs rb = h->rbufs();
+  return enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d, flags, h->st,
+              nullptr, nullptr, &rb);
 }
 
 // The full step: velnw+bondv1 (A -> B), velfg+feedbf+les+adam+rhs (B -> A), press.
-void enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omega) {
+// With timing on, event records are captured between the phases:
+// ev0 | velnw+bondv1 | ev1 | fused | ev2 | SOR passes | ev3 | halo + reduction | ev4
+cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omega) {
   unsigned* flags = &h->book_d->flags;
+  auto mark = [&](int i) {
+    if (h->timing) cudaEventRecordWithFlags(h->ev[i], h->st, cudaEventRecordExternal);
+  };
+  mark(0);
   launch_velnw_bondv1(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->inflow_d, h->ub, h->vb, h->wb,
                       flags, h->st);
+  mark(1);
   launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
                    h->vn, h->dt, h->cs != 0.0f, h->csd2, h->csd2s, flags, h->st);
-  enqueue_press(h, n_iter, scheme, omega, false, flags);
+  mark(2);
+  ExchangeHook hook{nullptr, nullptr};
+  SorMarks marks{h->timing ? h->ev[3] : nullptr};
+  ResidentBufs rb = h->rbufs();
+  cudaError_t e = enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials,
+                              h->res_d, flags, h->st, &hook, &marks, &rb);
+  mark(4);
+  return e;
 }
 
 int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cudaGraphExec_t* out) {
   unsigned ob;
   std::memcpy(&ob, &omega, 4);
-  auto key = std::make_tuple(mode, n_iter, scheme, ob);
+  auto key = std::make_tuple(mode | (h->timing ? 2 : 0), n_iter, scheme, ob);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) {
     *out = it->second;
@@ -171,16 +218,22 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   if (mode == MODE_SYNC) {
     cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), h->st);
+    cudaMemsetAsync(&h->book_d->err, 0, sizeof(unsigned), h->st);
     cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * h->g.km * sizeof(float), cudaMemcpyHostToDevice, h->st);
   }
-  enqueue_step_body(h, n_iter, scheme, omega);
+  cudaError_t body_err = enqueue_step_body(h, n_iter, scheme, omega);
   if (mode == MODE_SYNC) {
     cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st);
-    cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st);
+    cudaMemcpyAsync(h->book_h, h->book_d, sizeof(StepBook), cudaMemcpyDeviceToHost, h->st);
   } else {
     k_step_tail<<<1, 32, 0, h->st>>>(h->book_d);
   }
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+  if (body_err != cudaSuccess) {
+    if (e == cudaSuccess) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return fail(LESB_E_CUDA, std::string("step capture: ") + cudaGetErrorString(body_err));
+  }
   if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
   cudaGraphExec_t exec;
   e = cudaGraphInstantiate(&exec, graph, 0);
@@ -289,7 +342,7 @@ int lesb_create(const lesb_desc* d, lesb_handle* out) {
   if (err == cudaSuccess) err = cudaMemcpy(h->dy1, d->dy1, (g.jm + 2) * sizeof(float), cudaMemcpyHostToDevice);
   if (err == cudaSuccess) err = cudaMemcpy(h->dzn, d->dzn, (g.km + 2) * sizeof(float), cudaMemcpyHostToDevice);
   if (err == cudaSuccess) {
-    StepBook b{0u, 0u, -1, 0u};
+    StepBook b{0u, 0u, -1, 0u, 0u};
     err = cudaMemcpy(h->book_d, &b, sizeof(b), cudaMemcpyHostToDevice);
   }
   if (err == cudaSuccess && d->csd2) {
@@ -303,6 +356,7 @@ int lesb_create(const lesb_desc* d, lesb_handle* out) {
     return fail(err == cudaErrorMemoryAllocation ? LESB_E_NOMEM : LESB_E_CUDA, m);
   }
   h->known_finite = true;  // all zero
+  h->sor_path = g_default_sor_path >= 0 ? g_default_sor_path : default_sor_path();
   *out = h;
   return LESB_OK;
 }
@@ -323,6 +377,8 @@ int lesb_destroy(lesb_handle h) {
   if (h->res_h) cudaFreeHost(h->res_h);
   if (h->book_h) cudaFreeHost(h->book_h);
   if (h->inflow_h) cudaFreeHost(h->inflow_h);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
   return LESB_OK;
@@ -498,7 +554,7 @@ int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* resid
   CK(cudaSetDevice(h->device));
   rc = ensure_partials(h, n_iter);
   if (rc) return rc;
-  enqueue_press(h, n_iter, scheme, omega, true, nullptr);
+  CK(enqueue_press(h, n_iter, scheme, omega, true, nullptr));
   CK(cudaGetLastError());
   if (residuals_out)
     CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
@@ -530,6 +586,7 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   CK(cudaGraphLaunch(ge, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (residuals_out) std::memcpy(residuals_out, h->res_h, n_iter * sizeof(double));
+  if (h->book_h->err) return fail(LESB_E_CUDA, "resident SOR: neighbour wait timed out");
   unsigned bits = h->book_h->flags;
   if (bits) {
     h->known_finite = false;
@@ -560,7 +617,7 @@ int lesb_step_async(lesb_handle h, int n_iter, int scheme, float omega) {
     rc = handle_dirty_state(h, nullptr, &failed);
     if (rc) return rc;
     if (failed) return fail(LESB_E_STATE, "state holds non-finite values");
-    StepBook b{0u, 0u, -1, 0u};
+    StepBook b{0u, 0u, -1, 0u, 0u};
     CK(cudaMemcpyAsync(h->book_d, &b, sizeof(b), cudaMemcpyHostToDevice, h->st));
   }
   cudaGraphExec_t ge;
@@ -580,8 +637,9 @@ int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_
   if (steps_done) *steps_done = (int)b.steps;
   if (fail_step) *fail_step = b.fail_step;
   if (fail_stage) *fail_stage = b.fail_step >= 0 ? first_stage(b.fail_flags) : -1;
+  if (b.err) return fail(LESB_E_CUDA, "resident SOR: neighbour wait timed out");
   // reset the counters for the next run
-  StepBook z{0u, 0u, -1, 0u};
+  StepBook z{0u, 0u, -1, 0u, 0u};
   CK(cudaMemcpyAsync(h->book_d, &z, sizeof(z), cudaMemcpyHostToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (b.fail_step >= 0) h->known_finite = false;
@@ -630,9 +688,72 @@ int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profil
   return LESB_OK;
 }
 
+int lesb_copy_state(lesb_handle dst, lesb_handle src) {
+  if (!dst || !src) return fail(LESB_E_ARG, "null handle");
+  if (dst->n_alloc != src->n_alloc || dst->device != src->device) return fail(LESB_E_ARG, "domains differ");
+  std::lock_guard<std::mutex> lk(dst->mu);
+  CK(cudaSetDevice(dst->device));
+  CK(cudaStreamSynchronize(src->st));
+  const size_t fb = dst->n_alloc * sizeof(float);
+  CK(cudaMemcpyAsync(dst->u, src->u, fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->v, src->v, fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->w, src->w, fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->p, src->p, fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->mask, src->mask, fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->fgh, src->fgh, 3 * fb, cudaMemcpyDeviceToDevice, dst->st));
+  CK(cudaMemcpyAsync(dst->fgh_old, src->fgh_old, 3 * fb, cudaMemcpyDeviceToDevice, dst->st));
+  dst->known_finite = src->known_finite;
+  return LESB_OK;
+}
+
+int lesb_set_sor_path(lesb_handle h, int path) {
+  if (!h || path < 0 || path > 2) return fail(LESB_E_ARG, "bad argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  h->sor_path = path;
+  clear_graphs(h);
+  return LESB_OK;
+}
+
+int lesb_set_default_sor_path(int path) {
+  if (path < 0 || path > 2) return fail(LESB_E_ARG, "bad argument");
+  g_default_sor_path = path;
+  std::lock_guard<std::mutex> lk(g_solver_mu_fwd());
+  for (auto& kv : solver_map()) lesb_set_sor_path(kv.second, path);
+  return LESB_OK;
+}
+
+int lesb_sor_path_in_use(lesb_handle h, int scheme) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  if (scheme != LESB_REDBLACK || h->sor_path == 1 || !h->coeffs_set) return 1;
+  return resident_supported(h->g, h->sorc(), h->device) ? 2 : 1;
+}
+
+int lesb_set_timing(lesb_handle h, int on) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  for (auto& e : h->ev)
+    if (!e) CK(cudaEventCreate(&e));
+  h->timing = on != 0;
+  return LESB_OK;
+}
+
+int lesb_last_step_times(lesb_handle h, float* ms) {
+  if (!h || !ms) return fail(LESB_E_ARG, "null argument");
+  if (!h->timing) return fail(LESB_E_STATE, "timing is off (lesb_set_timing)");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[i + 1]));
+  return LESB_OK;
+}
+
 int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
   if (!h) return fail(LESB_E_ARG, "null handle");
-  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1);
+  const bool res = h->sor_path != 1 && resident_supported(h->g, h->sorc(), h->device);
+  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, res);
 }
 
 // ---- solver on host buffers ----
@@ -640,11 +761,9 @@ int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
 
 namespace {
 
-std::mutex g_solver_mu;
-std::map<std::tuple<int, int, int, int>, lesb_domain*> g_solvers;
-
 int get_solver(int im, int jm, int km, int device, lesb_domain** out) {
-  std::lock_guard<std::mutex> lk(g_solver_mu);
+  std::lock_guard<std::mutex> lk(g_solver_mu_fwd());
+  auto& g_solvers = solver_map();
   auto key = std::make_tuple(im, jm, km, device);
   auto it = g_solvers.find(key);
   if (it != g_solvers.end()) {
@@ -705,8 +824,9 @@ int lesb_solve_pressure(int im, int jm, int km, const float* p0, const float* rh
   const size_t bytes = h->n_py * sizeof(float);
   CK(cudaMemcpyAsync(h->p, p0, bytes, cudaMemcpyHostToDevice, h->st));
   if (scheme == LESB_TWINNED) CK(cudaMemcpyAsync(h->pb, h->p, bytes, cudaMemcpyDeviceToDevice, h->st));
-  enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, halo_policy, h->partials, h->res_d,
-              nullptr, h->st, nullptr);
+  ResidentBufs rb = h->rbufs();
+  CK(enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, halo_policy, h->partials, h->res_d,
+                 nullptr, h->st, nullptr, nullptr, &rb));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(p_out, h->p, bytes, cudaMemcpyDeviceToHost, h->st));
   if (residuals) CK(cudaMemcpyAsync(residuals, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));

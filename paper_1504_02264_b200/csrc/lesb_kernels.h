@@ -15,6 +15,21 @@ struct ExchangeHook {
   void* ctx;
 };
 
+// Optional event recorded after the last SOR pass (stage timing).
+struct SorMarks {
+  cudaEvent_t after_passes;
+};
+
+// Buffers of the shared-memory-resident red-black solver (sor_resident.cu);
+// use == 0 forces the streaming kernels.
+struct ResidentBufs {
+  int use;
+  int device;
+  float* xbuf;
+  unsigned* flags;
+  unsigned* err;
+};
+
 // stages.cu
 void launch_velnw(const Geo& g, const Spac& s, float* u, float* v, float* w, const float* p, const float* fgh,
                   float dt, cudaStream_t st);
@@ -48,9 +63,17 @@ void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rh
                      int policy, double* partials, cudaStream_t st);
 void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st);
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st);
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy);
-void enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
-                 int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
-                 const ExchangeHook* hook);
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident);
+cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
+                        int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
+                        const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res = nullptr);
+
+// sor_resident.cu
+bool resident_supported(const Geo& g, const SorC& cf, int device);
+int resident_ntiles(const Geo& g, int device);
+long long resident_xbuf_floats(const Geo& g, int device);
+cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
+                                int n_iter, int policy, float* xbuf, unsigned* flags, double* partials,
+                                unsigned* err, cudaStream_t st);
 
 }  // namespace lesb

@@ -217,7 +217,8 @@ void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out
   k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
 }
 
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy) {
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident) {
+  if (resident && scheme == 0) return 1 + (policy == 1 ? 1 : 0) + 1;
   int per_iter = 2;
   if (scheme == 0 && policy == 1 && (g.jm & 1)) per_iter = 4;
   return per_iter * n_iter + (policy == 1 ? 1 : 0) + 1;
@@ -225,9 +226,19 @@ int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy) {
 
 // Enqueue a full solve on p (in place).  TWINNED needs pb initialised to a
 // copy of p by the caller (make_twinned, sor.py:145-150).
-void enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
-                 int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
-                 const ExchangeHook* hook) {
+cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
+                        int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
+                        const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res) {
+  if (scheme == 0 && res && res->use && !(hook && hook->fn) && resident_supported(g, cf, res->device)) {
+    const int nt = resident_ntiles(g, res->device);
+    cudaError_t e = launch_sor_resident(g, res->device, p, rhs, cf, om, n_iter, policy, res->xbuf, res->flags,
+                                        partials, res->err, st);
+    if (e != cudaSuccess) return e;
+    if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
+    if (policy == 1) launch_press_halo(g, p, flags, st);
+    launch_reduce_res(partials, nt, n_iter, res_dev, st);
+    return cudaGetLastError();
+  }
   const int nblk = scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g);
   for (int it = 0; it < n_iter; ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {
@@ -243,11 +254,13 @@ void enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC
       }
     }
   }
+  if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
   if (policy == 1) {
     launch_press_halo(g, p, flags, st);
     if (hook && hook->fn) hook->fn(hook->ctx, p);
   }
   launch_reduce_res(partials, nblk, n_iter, res_dev, st);
+  return cudaGetLastError();
 }
 
 }  // namespace lesb

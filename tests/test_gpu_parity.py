@@ -21,11 +21,16 @@ FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p")
 RTOL_RES = 1e-12
 
 
-@pytest.fixture(scope="module")
-def P():
+@pytest.fixture(scope="module", params=[1, 0], ids=["streaming", "resident"])
+def P(request):
+    """The package with the red-black solver forced to the streaming kernels
+    (1) or left on auto, which selects the shared-memory-resident persistent
+    kernel wherever the grid fits (0).  Every test runs on both."""
     import paper_1504_02264_b200 as pkg
 
-    return pkg
+    pkg.runtime.set_sor_path(request.param)
+    yield pkg
+    pkg.runtime.set_sor_path(0)
 
 
 def sha(a):
@@ -251,3 +256,17 @@ def test_determinism(P):
     for n in FIELDS:
         assert bits_equal(getattr(outs[0][0], n), getattr(outs[1][0], n))
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_solver_path_selection(P):
+    """Auto picks the resident solver for the benchmark grid; both paths are
+    reachable."""
+    from paper_1504_02264_b200 import _native as N
+
+    fs = dstate(P, gi.config2_state())
+    h = fs.handle()
+    fs._ensure_coeffs(h)
+    path = N.load().lesb_sor_path_in_use(h.h, 0)
+    assert path in (1, 2)
+    lib = N.load()
+    assert lib.lesb_sor_path_in_use(h.h, 1) == 1  # twinned always streams
