@@ -94,6 +94,8 @@ struct lesb_domain {
   float* cn1 = nullptr;
   float* cn[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   float cn1s = 0.f;
+  int cuni = 0;
+  float cw[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   bool coeffs_set = false;
   float* inflow_d = nullptr;
   float* inflow_h = nullptr;  // pinned
@@ -107,9 +109,9 @@ struct lesb_domain {
   float* scratch = nullptr;  // im*jm*km
   std::map<std::tuple<int, int, int, unsigned>, cudaGraphExec_t> graphs;
   bool timing = false;
-  int sor_path = 0;  // 0 auto, 1 streaming kernels, 2 shared-memory-resident solver
-  float* xbuf = nullptr;
-  unsigned* rflags = nullptr;
+  int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 colour-fused streaming
+  void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
+  unsigned* repoch = nullptr;  // resident solver tag epoch
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool known_finite = false;
   long long n_alloc = 0;  // (im+3)*si
@@ -117,8 +119,14 @@ struct lesb_domain {
   std::mutex mu;
 
   Spac spac() const { return Spac{dx1, dy1, dzn}; }
-  SorC sorc() const { return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5]}; }
-  ResidentBufs rbufs() const { return ResidentBufs{sor_path != 1 && xbuf != nullptr, device, xbuf, rflags, &book_d->err}; }
+  SorC sorc() const {
+    return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5], cuni, cw[0], cw[1], cw[2], cw[3], cw[4], cw[5]};
+  }
+  ResidentBufs rbufs() const {
+    const bool res = (sor_path == 0 || sor_path == 2) && xbuf != nullptr;
+    const bool fz = sor_path == 3 || (sor_path == 0 && !res);
+    return ResidentBufs{res, device, fz ? 1 : 0, xbuf, repoch, &book_d->err};
+  }
   long long n_int() const { return (long long)g.im * g.jm * g.km; }
 };
 
@@ -126,16 +134,20 @@ namespace {
 
 int ensure_partials(lesb_domain* h, int n_iter) {
   long long need = (long long)n_iter * 2 *
-                   std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_ntiles(h->g, h->device));
+                   std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_partials(h->g, h->device)),
+                            sor_blocks_fused(h->g, h->device));
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
     h->partials = nullptr;
     CK(cudaMalloc(&h->partials, need * sizeof(double)));
     h->partials_cap = need;
   }
-  if (h->sor_path != 1 && !h->xbuf && resident_supported(h->g, h->sorc(), h->device)) {
-    CK(cudaMalloc(&h->xbuf, resident_xbuf_floats(h->g, h->device) * sizeof(float)));
-    CK(cudaMalloc(&h->rflags, resident_ntiles(h->g, h->device) * sizeof(unsigned)));
+  if ((h->sor_path == 0 || h->sor_path == 2) && !h->xbuf && resident_supported(h->g, h->sorc(), h->device)) {
+    const size_t xb = resident_xbuf_words(h->g, h->device) * sizeof(unsigned long long);
+    CK(cudaMalloc(&h->xbuf, xb));
+    CK(cudaMemset(h->xbuf, 0, xb));
+    CK(cudaMalloc(&h->repoch, sizeof(unsigned)));
+    CK(cudaMemset(h->repoch, 0, sizeof(unsigned)));
   }
   if (n_iter > h->res_cap) {
     if (h->res_d) cudaFree(h->res_d);
@@ -147,6 +159,24 @@ int ensure_partials(lesb_domain* h, int n_iter) {
     h->res_cap = n_iter;
   }
   return LESB_OK;
+}
+
+// A resident solve whose neighbour wait timed out leaves its tile flags set:
+// clear them (and the error word) so the next solve starts clean.
+int resident_timeout(lesb_domain* h) {
+  cudaStreamSynchronize(h->st);
+  if (h->xbuf) cudaMemset(h->xbuf, 0, resident_xbuf_words(h->g, h->device) * sizeof(unsigned long long));
+  if (h->repoch) cudaMemset(h->repoch, 0, sizeof(unsigned));
+  cudaMemset(&h->book_d->err, 0, sizeof(unsigned));
+  cudaDeviceSynchronize();
+  return fail(LESB_E_CUDA, "resident SOR: neighbour wait timed out");
+}
+
+// After a synchronous solve: report a resident-solver wait timeout.
+int check_resident_err(lesb_domain* h) {
+  unsigned e = 0;
+  CK(cudaMemcpy(&e, &h->book_d->err, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  return e ? resident_timeout(h) : LESB_OK;
 }
 
 void clear_graphs(lesb_domain* h) {
@@ -372,6 +402,8 @@ int lesb_destroy(lesb_handle h) {
   for (float* b : bufs)
     if (b) cudaFree(b);
   if (h->partials) cudaFree(h->partials);
+  if (h->xbuf) cudaFree(h->xbuf);
+  if (h->repoch) cudaFree(h->repoch);
   if (h->res_d) cudaFree(h->res_d);
   if (h->book_d) cudaFree(h->book_d);
   if (h->res_h) cudaFreeHost(h->res_h);
@@ -392,6 +424,13 @@ int lesb_set_coeffs(lesb_handle h, const lesb_coeffs* c) {
   const Geo& g = h->g;
   const int lens[6] = {g.im, g.im, g.jm, g.jm, g.km, g.km};
   const float* src[6] = {c->cn2l, c->cn2s, c->cn3l, c->cn3s, c->cn4l, c->cn4s};
+  h->cuni = 1;
+  for (int a = 0; a < 6; ++a) {
+    if (!src[a]) return fail(LESB_E_ARG, "cn2l/cn2s/cn3l/cn3s/cn4l/cn4s are required");
+    h->cw[a] = src[a][0];
+    for (int x = 1; x < lens[a]; ++x)
+      if (std::memcmp(&src[a][x], &src[a][0], sizeof(float)) != 0) h->cuni = 0;
+  }
   for (int a = 0; a < 6; ++a) {
     if (!src[a]) return fail(LESB_E_ARG, "cn2l/cn2s/cn3l/cn3s/cn4l/cn4s are required");
     if (!h->cn[a]) CK(cudaMalloc(&h->cn[a], lens[a] * sizeof(float)));
@@ -559,6 +598,8 @@ int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* resid
   if (residuals_out)
     CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  rc = check_resident_err(h);
+  if (rc) return rc;
   h->known_finite = false;
   return LESB_OK;
 }
@@ -586,7 +627,7 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   CK(cudaGraphLaunch(ge, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (residuals_out) std::memcpy(residuals_out, h->res_h, n_iter * sizeof(double));
-  if (h->book_h->err) return fail(LESB_E_CUDA, "resident SOR: neighbour wait timed out");
+  if (h->book_h->err) return resident_timeout(h);
   unsigned bits = h->book_h->flags;
   if (bits) {
     h->known_finite = false;
@@ -637,7 +678,7 @@ int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_
   if (steps_done) *steps_done = (int)b.steps;
   if (fail_step) *fail_step = b.fail_step;
   if (fail_stage) *fail_stage = b.fail_step >= 0 ? first_stage(b.fail_flags) : -1;
-  if (b.err) return fail(LESB_E_CUDA, "resident SOR: neighbour wait timed out");
+  if (b.err) return resident_timeout(h);
   // reset the counters for the next run
   StepBook z{0u, 0u, -1, 0u, 0u};
   CK(cudaMemcpyAsync(h->book_d, &z, sizeof(z), cudaMemcpyHostToDevice, h->st));
@@ -707,7 +748,7 @@ int lesb_copy_state(lesb_handle dst, lesb_handle src) {
 }
 
 int lesb_set_sor_path(lesb_handle h, int path) {
-  if (!h || path < 0 || path > 2) return fail(LESB_E_ARG, "bad argument");
+  if (!h || path < 0 || path > 3) return fail(LESB_E_ARG, "bad argument");
   std::lock_guard<std::mutex> lk(h->mu);
   CK(cudaSetDevice(h->device));
   CK(cudaStreamSynchronize(h->st));
@@ -717,7 +758,7 @@ int lesb_set_sor_path(lesb_handle h, int path) {
 }
 
 int lesb_set_default_sor_path(int path) {
-  if (path < 0 || path > 2) return fail(LESB_E_ARG, "bad argument");
+  if (path < 0 || path > 3) return fail(LESB_E_ARG, "bad argument");
   g_default_sor_path = path;
   std::lock_guard<std::mutex> lk(g_solver_mu_fwd());
   for (auto& kv : solver_map()) lesb_set_sor_path(kv.second, path);
@@ -727,7 +768,10 @@ int lesb_set_default_sor_path(int path) {
 int lesb_sor_path_in_use(lesb_handle h, int scheme) {
   if (!h) return fail(LESB_E_ARG, "null handle");
   if (scheme != LESB_REDBLACK || h->sor_path == 1 || !h->coeffs_set) return 1;
-  return resident_supported(h->g, h->sorc(), h->device) ? 2 : 1;
+  const bool res = (h->sor_path == 0 || h->sor_path == 2) && resident_supported(h->g, h->sorc(), h->device);
+  if (res) return 2;
+  if ((h->sor_path == 0 || h->sor_path == 3) && fused_supported(h->g, h->sorc(), h->device)) return 3;
+  return 1;
 }
 
 int lesb_set_timing(lesb_handle h, int on) {
@@ -752,8 +796,8 @@ int lesb_last_step_times(lesb_handle h, float* ms) {
 
 int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
   if (!h) return fail(LESB_E_ARG, "null handle");
-  const bool res = h->sor_path != 1 && resident_supported(h->g, h->sorc(), h->device);
-  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, res);
+  const int path = lesb_sor_path_in_use(h, scheme);
+  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, path == 2, path == 3);
 }
 
 // ---- solver on host buffers ----
@@ -831,7 +875,7 @@ int lesb_solve_pressure(int im, int jm, int km, const float* p0, const float* rh
   CK(cudaMemcpyAsync(p_out, h->p, bytes, cudaMemcpyDeviceToHost, h->st));
   if (residuals) CK(cudaMemcpyAsync(residuals, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  return LESB_OK;
+  return check_resident_err(h);
 }
 
 int lesb_redblack_iteration(int im, int jm, int km, float* p, const float* rhs, const lesb_coeffs* c, float omega,

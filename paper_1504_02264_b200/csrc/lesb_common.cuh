@@ -40,6 +40,10 @@ struct SorC {
   const float* cn1;  // im*jm*km (interior, C order) or nullptr -> cn1s
   float cn1s;
   const float *cn2l, *cn2s, *cn3l, *cn3s, *cn4l, *cn4s;
+  // uni != 0: every entry of each neighbour-weight vector equals the scalar
+  // below (build_uniform_coeffs, sor.py:121-137), so kernels may use them.
+  int uni;
+  float w2l, w2s, w3l, w3s, w4l, w4s;
 };
 
 __device__ __forceinline__ bool finite32(float x) {

@@ -25,8 +25,9 @@ struct SorMarks {
 struct ResidentBufs {
   int use;
   int device;
-  float* xbuf;
-  unsigned* flags;
+  int fused;         // use the colour-fused streaming kernel (when the resident one is not used)
+  void* xbuf;        // resident_xbuf_words() 64-bit words, zero-initialised
+  unsigned* epoch;   // one word, zero-initialised
   unsigned* err;
 };
 
@@ -62,18 +63,38 @@ void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, fl
 void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rhs, const SorC& cf, float om,
                      int policy, double* partials, cudaStream_t st);
 void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st);
+void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned* flags, cudaStream_t st);
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st);
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident);
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused);
 cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
                         int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
                         const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res = nullptr);
 
+// sor_fused.cu
+bool fused_supported(const Geo& g, const SorC& cf, int device);
+int sor_blocks_fused(const Geo& g, int device);
+cudaError_t launch_rb_fused(const Geo& g, int device, const float* pa, float* pb, const float* rhs, const SorC& cf,
+                            float om, int policy, double* partials, cudaStream_t st);
+
 // sor_resident.cu
 bool resident_supported(const Geo& g, const SorC& cf, int device);
 int resident_ntiles(const Geo& g, int device);
-long long resident_xbuf_floats(const Geo& g, int device);
+int resident_partials(const Geo& g, int device);  // per-pass residual partials
+long long resident_xbuf_words(const Geo& g, int device);
 cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
-                                int n_iter, int policy, float* xbuf, unsigned* flags, double* partials,
-                                unsigned* err, cudaStream_t st);
+                                int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
+                                double* res, unsigned* pflags, unsigned* err, cudaStream_t st);
+
+// sor_regrun.cu (register-run variant, chosen by launch_sor_resident when it fits)
+struct RRPlanView {
+  int ntiles;
+  long long xbuf;
+  int partials;  // per-pass residual partials
+  bool ok;
+};
+RRPlanView regrun_view(const Geo& g, int device);
+cudaError_t launch_sor_regrun(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
+                              int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials, double* res,
+                              unsigned* pflags, unsigned* err, cudaStream_t st);
 
 }  // namespace lesb

@@ -123,9 +123,11 @@ __global__ void k_refresh_y(Geo g, float* __restrict__ p) {
 }
 
 // Final halo_fn(p) of the press policy in closed form: resolve k (0 -> 1,
-// km+1 -> 0), then j (periodic), then i (0 -> 1, im+1 -> 0).  Optionally
-// checks every cell of p for finiteness (press stage, les.py:413-415).
-__global__ void k_press_halo(Geo g, float* __restrict__ p, unsigned* flags) {
+// km+1 -> 0), then j (periodic), then i (0 -> 1, im+1 -> 0).  Reads src and
+// writes the whole array to dst (src == dst: in place; halo sources are
+// interior cells, which are not written).  Optionally checks every cell of
+// the result for finiteness (press stage, les.py:413-415).
+__global__ void k_press_halo(Geo g, const float* src, float* dst, unsigned* flags) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   const int i = blockIdx.z;
@@ -142,11 +144,12 @@ __global__ void k_press_halo(Geo g, float* __restrict__ p, unsigned* flags) {
         const int kk = k == 0 ? 1 : k;
         const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
         const int ii = i == 0 ? 1 : i;
-        val = p[cidx(g, ii, jj, kk)];
+        val = src[cidx(g, ii, jj, kk)];
       }
-      p[c] = val;
+      dst[c] = val;
     } else {
-      val = p[c];
+      val = src[c];
+      if (src != dst) dst[c] = val;
     }
     if (flags && !finite32(val)) bits = F_PRESS;
   }
@@ -205,20 +208,25 @@ void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rh
 }
 
 void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st) {
+  launch_press_halo_copy(g, p, p, flags, st);
+}
+
+void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned* flags, cudaStream_t st) {
   int nk = g.km + 2;
   int bx = ((nk + 31) / 32) * 32;
   if (bx > 128) bx = 128;
   int by = 256 / bx;
   dim3 grid((nk + bx - 1) / bx, (g.jm + 2 + by - 1) / by, g.im + 2);
-  k_press_halo<<<grid, dim3(bx, by), 0, st>>>(g, p, flags);
+  k_press_halo<<<grid, dim3(bx, by), 0, st>>>(g, src, dst, flags);
 }
 
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st) {
   k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
 }
 
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident) {
-  if (resident && scheme == 0) return 1 + (policy == 1 ? 1 : 0) + 1;
+int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused) {
+  if (resident && scheme == 0) return 1;
+  if (fused && scheme == 0) return n_iter + (policy == 1 || (n_iter & 1) ? 1 : 0) + 1;
   int per_iter = 2;
   if (scheme == 0 && policy == 1 && (g.jm & 1)) per_iter = 4;
   return per_iter * n_iter + (policy == 1 ? 1 : 0) + 1;
@@ -230,13 +238,30 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
                         int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
                         const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res) {
   if (scheme == 0 && res && res->use && !(hook && hook->fn) && resident_supported(g, cf, res->device)) {
-    const int nt = resident_ntiles(g, res->device);
-    cudaError_t e = launch_sor_resident(g, res->device, p, rhs, cf, om, n_iter, policy, res->xbuf, res->flags,
-                                        partials, res->err, st);
+    // one launch: passes, press halo + its non-finite check, residuals
+    cudaError_t e = launch_sor_resident(g, res->device, p, rhs, cf, om, n_iter, policy, res->xbuf, res->epoch,
+                                        partials, res_dev, flags, res->err, st);
     if (e != cudaSuccess) return e;
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
-    if (policy == 1) launch_press_halo(g, p, flags, st);
-    launch_reduce_res(partials, nt, n_iter, res_dev, st);
+    return cudaGetLastError();
+  }
+  if (scheme == 0 && res && res->fused && !(hook && hook->fn) && fused_supported(g, cf, res->device)) {
+    // colour-fused out-of-place iterations, ping-pong p <-> pb
+    const int nb = sor_blocks_fused(g, res->device);
+    const size_t bytes = (size_t)(g.im + 2) * g.si * sizeof(float);
+    cudaError_t e = cudaMemcpyAsync(pb, p, bytes, cudaMemcpyDeviceToDevice, st);  // pb's halo = stored halo
+    if (e != cudaSuccess) return e;
+    for (int it = 0; it < n_iter; ++it) {
+      const float* src = (it & 1) ? pb : p;
+      float* dst = (it & 1) ? p : pb;
+      e = launch_rb_fused(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st);
+      if (e != cudaSuccess) return e;
+    }
+    if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
+    float* fin = (n_iter & 1) ? pb : p;
+    if (policy == 1) launch_press_halo_copy(g, fin, p, flags, st);
+    else if (fin != p) cudaMemcpyAsync(p, fin, bytes, cudaMemcpyDeviceToDevice, st);
+    launch_reduce_res(partials, nb, n_iter, res_dev, st);
     return cudaGetLastError();
   }
   const int nblk = scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g);

@@ -1,5 +1,7 @@
 // Persistent, shared-memory-resident red-black SOR (reference semantics:
-// gmcf_mini/sor.py:181-203 with the halo policies of sor.cu).
+// gmcf_mini/sor.py:181-203 with the halo policies of sor.cu, plus the final
+// halo_fn call of the press policy, les.py:341-355, and the residual sums of
+// sor.py:199-203).
 //
 // One CTA per SM (cooperative launch, so every CTA is co-resident) owns an
 // (i, j) tile of the grid with its full k columns.  The tile's pressure and
@@ -7,34 +9,54 @@
 // L2, once per colour pass:
 //
 //   for pass n (colour nrd = n & 1):
-//     update the colour-nrd cells of the tile in shared memory
-//     publish the colour-nrd cells of the 4 tile faces to a global face buffer
-//     release-store flag[tile] = n + 1
+//     update the colour-nrd cells of the tile's BOUNDARY columns
+//     publish their colour-nrd values to a global face buffer, release flag
+//     update the colour-nrd cells of the tile's INTERIOR columns (this hides
+//       the latency of the publish / flag round trip)
 //     acquire-wait until every neighbour's flag >= n + 1
-//     copy the neighbours' published faces into the tile's halo slots
+//     copy the neighbours' published faces into the tile's halo columns
 //
-// Shared memory holds each colour separately ("colour split": cell (i,j,k)
-// lives in array colour(i,j,k) at slot k >> 1), so a warp's 32 lanes touch 32
-// consecutive words for the centre, all six neighbours and rhs (no bank
-// conflicts).  Halo slots take the colour of their storage position; for the
+// Layout ("colour split"): cell (i,j,k) lives in colour array
+// colour(i,j,k) = (i+j+k+1)&1 at slot k>>1 of its column, so for a fixed
+// column the colour-c cells are consecutive slots and a warp's lanes touch
+// consecutive words for the centre, all six neighbours and rhs.  With
+// kp = parity of the colour's k values in the column and t = 0,1,...:
+//   k = 2t + 2 - kp, centre slot t + 1 - kp, top slot t + 1, bottom slot t,
+// so every address is (column base + t + constant).
+//
+// Work items (column, t) are walked with an incremental decode (no integer
+// division in the pass loop) over a column table whose boundary columns come
+// first.  Halo slots take the colour of their storage position; for the
 // periodic wrap with odd jm the source cell has the other colour, which is
 // exactly the reference's pre-pass snapshot of the y halo (the slot is only
 // refreshed after the pass that updated its source).
+//
+// After the last pass each tile writes its columns back, materialising the
+// press halo in closed form for the halo cells whose
+// source it owns and raising the press non-finite bit; after a grid-wide
+// barrier tile b reduces the residual of iteration b in a fixed order.
 //
 // Arithmetic per point is sor_point's (same op order, -fmad=false), so the
 // result is bitwise identical to the streaming kernels and the reference.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace lesb {
+
+constexpr int RES_THREADS = 512;
+constexpr int RES_WARPS = RES_THREADS / 32;
 
 struct ResPlan {
   int ni, nj;       // tile grid
   int ti_max, tj_max;
   int kk;           // slots per colour column: ((km + 1) >> 1) + 1
-  int nthreads;
+  int kt;           // work items per column and pass: (km + 1) >> 1
   size_t smem;      // dynamic shared memory bytes
   long long xbuf;   // floats of the face exchange buffer
   bool ok;
@@ -45,213 +67,385 @@ struct ResArgs {
   ResPlan pl;
   float* p;
   const float* rhs;
-  SorC cf;
-  float om;
+  float om, cn1;
+  float w2l, w2s, w3l, w3s, w4l, w4s;
   int n_iter;
-  int policy;       // 0 STORED, 1 PRESS
-  float* xbuf;      // [2][ntiles][4][fmax * kk]
-  unsigned* flags;  // [ntiles], zero at entry
-  double* partials; // [2 n_iter][ntiles]
-  unsigned* err;    // set when a neighbour wait times out
+  unsigned long long* xbuf;  // [4][ntiles][4][fmax * kk] (value, tag) words, ring of 4 passes
+  unsigned* epoch;   // launch counter: tags of this launch are unique across launches
+  double* partials;  // [2 n_iter][ntiles][RES_WARPS] per-warp residual partials
+  double* res;       // [n_iter] residual per iteration
+  unsigned* pflags;  // stage flag word (F_PRESS) or nullptr
+  unsigned* err;     // set when a neighbour wait times out
+  int debug;         // timing experiments only (LESB_RES_DEBUG): 1 no waits, 2 no updates, 4 no receive
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
+// Face exchange in the "LL" style: every published value travels with the
+// tag of its pass in one 64-bit word, written and read with single-copy-atomic
+// 64-bit accesses, so a reader that sees the right tag also sees the right
+// value -- no fences, counters or flag round trips.
+__device__ __forceinline__ void st_ll(unsigned long long* a, float v, unsigned tag) {
+  const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w) : "memory");
 }
-__device__ __forceinline__ void st_release(unsigned* a, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+__device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a) : "memory");
+  return w;
 }
 
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
 
-// colour of global cell: the pass nrd updates cells with colour == nrd
+// colour of a cell: the pass nrd updates cells with colour == nrd
 // ((i-1)+(j-1)+(k-1)+nrd even, sor.py:174-178)
 __device__ __forceinline__ int colour(int i, int j, int k) { return (i + j + k + 1) & 1; }
 
-__global__ void __launch_bounds__(512, 1) k_sor_resident(ResArgs a) {
+// Shared-memory column layout: [p colour 0 | p colour 1 | rhs colour 0 |
+// rhs colour 1], KK slots each, so one column is 4 KK floats and every
+// operand of a point update is (column base + slot + a per-pass constant).
+// Column-table entry: column base | parity(i+j) << 28 | west-physical << 29.
+constexpr unsigned CB_MASK = 0x0FFFFFFFu;
+
+// One run of work: colour-nrd cells t0 <= t < t1 of one column.  The
+// addresses of consecutive cells differ by one slot, and the bottom neighbour
+// of cell t+1 is the top neighbour of cell t, so a run costs 7 shared loads
+// and 1 store per cell with no per-cell index arithmetic.
+template <bool PRESS, bool PUBLISH>
+__device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigned ci, int4 pub,
+                                             unsigned long long* X, unsigned tag, int t0, int t1, int nrd,
+                                             int KK, int CW, int sI, int km) {
+  const int cb = (int)(ci & CB_MASK);
+  const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
+  const bool wphys = PRESS && (ci & (1u << 29));
+  // cells k = 2t + 2 - kp <= km
+  const int tmax = (km + kp - 2) >> 1;  // last valid t
+  if (t1 > tmax + 1) t1 = tmax + 1;
+  float* cur = S + cb + nrd * KK + (1 - kp) + t0;           // centre, slot t + 1 - kp
+  const float* oth = S + cb + (1 - nrd) * KK + (1 - kp) + t0;  // other colour, same k
+  const float* tb = S + cb + (1 - nrd) * KK + t0;             // other colour, slot t (bottom)
+  const float* rr = cur + 2 * KK;
+  double acc = 0.0;
+  if (t0 >= t1) return acc;
+  float pB = tb[0];
+  int sl = t0 + 1 - kp;
+  for (int t = t0; t < t1; ++t) {
+    const float pc = *cur;
+    const float pE = oth[sI];
+    float pW = oth[-sI];
+    const float pN = oth[CW];
+    const float pS = oth[-CW];
+    const float pT = tb[1];
+    const float r = *rr;
+    float pb = pB;
+    if (PRESS) {
+      if (wphys) pW = pc;                   // physical west: p[0] -> p[1]
+      if (t == 0 && kp == 1) pb = pc;       // bottom: p[.,.,0] -> p[.,.,1]
+    }
+    // sor.py:164-171: E, W, N, S, T, B summed left to right
+    float nb = a.w2l * pE;
+    nb = nb + a.w2s * pW;
+    nb = nb + a.w3l * pN;
+    nb = nb + a.w3s * pS;
+    nb = nb + a.w4l * pT;
+    nb = nb + a.w4s * pb;
+    // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+    const float rel = a.om * (a.cn1 * (nb - r) - pc);
+    const float np = pc + rel;
+    *cur = np;
+    if (PUBLISH) {
+      if (pub.x >= 0) st_ll(X + pub.x + sl, np, tag);
+      if (pub.y >= 0) st_ll(X + pub.y + sl, np, tag);
+      if (pub.z >= 0) st_ll(X + pub.z + sl, np, tag);
+      if (pub.w >= 0) st_ll(X + pub.w + sl, np, tag);
+    }
+    acc += (double)rel * (double)rel;
+    pB = pT;
+    ++cur;
+    ++oth;
+    ++tb;
+    ++rr;
+    ++sl;
+  }
+  return acc;
+}
+
+// All runs of this thread in columns [c0, c1): the columns are cut into nseg
+// runs of L cells and run u = (c - c0) * nseg + g goes to thread u % nth.
+template <bool PRESS, bool PUBLISH>
+__device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
+                                               const int4* __restrict__ pubcol, unsigned long long* X,
+                                               unsigned tag, int c0, int c1, int nseg, int L, int KT, int nrd,
+                                               int KK, int CW, int sI, int km) {
+  double acc = 0.0;
+  const int nunits = (c1 - c0) * nseg;
+  for (int u = threadIdx.x; u < nunits; u += RES_THREADS) {
+    const int cc = u / nseg, g = u - cc * nseg;
+    const int c = c0 + cc;
+    const int t0 = g * L;
+    const int t1 = min(t0 + L, KT);
+    const int4 pub = PUBLISH ? pubcol[c] : make_int4(-1, -1, -1, -1);
+    acc += update_run<PRESS, PUBLISH>(a, S, coltab[c], pub, X, tag, t0, t1, nrd, KK, CW, sI, km);
+  }
+  return acc;
+}
+
+template <bool PRESS>
+__global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   extern __shared__ float smem[];
+  __shared__ double red[RES_WARPS];
   const Geo& g = a.g;
   const ResPlan& pl = a.pl;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x, nth = RES_THREADS;
+  const int lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x;
+  const int ntiles = pl.ni * pl.nj;
   const int ti = tile / pl.nj, tj = tile % pl.nj;
   const int I0 = tile_lo(ti, g.im, pl.ni), I1 = tile_lo(ti + 1, g.im, pl.ni);
   const int J0 = tile_lo(tj, g.jm, pl.nj), J1 = tile_lo(tj + 1, g.jm, pl.nj);
   const int TI = I1 - I0, TJ = J1 - J0;
-  const int KK = pl.kk;
-  const int sJ = KK, sI = (pl.tj_max + 2) * KK;
-  const int csz = (pl.ti_max + 2) * sI;  // floats per colour array
-  float* S = smem;                       // [2][ti_max+2][tj_max+2][KK]
-  float* R = smem + 2 * csz;             // same layout, interior used
+  const int KK = pl.kk, KT = pl.kt, km = g.km;
+  const int CW = 4 * KK + 1;                 // floats per column (odd: lanes in different columns spread over banks)
+  const int sI = (TJ + 2) * CW;              // column stride along i
+  const int ncol_h_max = (pl.ti_max + 2) * (pl.tj_max + 2);
+  float* S = smem;                           // [ti+2][tj+2][4][KK]
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
+  unsigned* coltab = reinterpret_cast<unsigned*>(smem + (((long long)ncol_h_max * CW + 3) & ~3LL));   // [TI*TJ]
+  int4* pubcol = reinterpret_cast<int4*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
+  int4* rcvtab = pubcol + pl.ti_max * pl.tj_max;                                      // [2TI+2TJ]
   const long long fstride = (long long)fmax * KK;
-  const int ntiles = pl.ni * pl.nj;
-  const bool press = a.policy == 1;
+  const long long tstride = 4 * fstride;     // words per tile in one face buffer
+  const long long bstride = tstride * ntiles;  // words per face buffer
 
-  // local (li, lj) in [0, TI+1] x [0, TJ+1]; global i = I0 - 1 + li
-  auto sidx = [&](int li, int lj, int k) { return li * sI + lj * sJ + (k >> 1); };
-  auto gval = [&](int i, int j, int k) { return a.p[cidx(g, i, j, k)]; };
+  auto colbase = [&](int li, int lj) { return (li * (TJ + 2) + lj) * CW; };
 
-  // ---- load tile interior, rhs and halo slots from global memory ----
-  const int ncol_h = (TI + 2) * (TJ + 2);
-  for (int idx = tid; idx < ncol_h * (g.km + 2); idx += nth) {
-    const int col = idx / (g.km + 2), k = idx - col * (g.km + 2);
-    const int li = col / (TJ + 2), lj = col - li * (TJ + 2);
-    const int i = I0 - 1 + li, j = J0 - 1 + lj;
-    const bool ih = li == 0 || li == TI + 1, jh = lj == 0 || lj == TJ + 1, kh = k == 0 || k == g.km + 1;
-    if ((ih && jh) || (ih && kh) || (jh && kh)) continue;  // edges/corners are never read
-    float v;
-    if (!press) {
-      v = gval(i, j, k);  // stored halo, or neighbour tile's initial value
-    } else if (kh) {
-      v = 0.0f;  // top: 0; bottom: remapped at read time
-    } else if (ih && (i == 0 || i == g.im + 1)) {
-      v = 0.0f;  // east: 0; west: remapped at read time
-    } else if (jh) {
-      const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
-      v = gval(i, jj, k);
-    } else {
-      v = gval(i, j, k);
-    }
-    S[colour(i, j, k) * csz + sidx(li, lj, k)] = v;
-    if (!ih && !jh && !kh) R[colour(i, j, k) * csz + sidx(li, lj, k)] = a.rhs[cidx(g, i, j, k)];
-  }
   // neighbour tiles (-1: physical boundary with a fixed / remapped halo)
   int nbr[4];
-  nbr[0] = ti > 0 ? tile - pl.nj : -1;            // west  <- its i-hi face
-  nbr[1] = ti < pl.ni - 1 ? tile + pl.nj : -1;    // east  <- its i-lo face
-  nbr[2] = tj > 0 ? tile - 1 : (press ? ti * pl.nj + pl.nj - 1 : -1);  // south <- its j-hi face
-  nbr[3] = tj < pl.nj - 1 ? tile + 1 : (press ? ti * pl.nj : -1);     // north <- its j-lo face
-  const int wrap_flip = (g.jm & 1);  // periodic source parity differs from the slot's for odd jm
-  __syncthreads();
+  nbr[0] = ti > 0 ? tile - pl.nj : -1;                                    // west  <- its east face (1)
+  nbr[1] = ti < pl.ni - 1 ? tile + pl.nj : -1;                            // east  <- its west face (0)
+  nbr[2] = tj > 0 ? tile - 1 : (PRESS ? ti * pl.nj + pl.nj - 1 : -1);     // south <- its north face (3)
+  nbr[3] = tj < pl.nj - 1 ? tile + 1 : (PRESS ? ti * pl.nj : -1);         // north <- its south face (2)
+  const int wrap_flip = g.jm & 1;  // periodic source parity differs from the slot's for odd jm
 
-  const int KH = (g.km + 1) >> 1;  // colour cells per column (upper bound)
+  // ---- tables: columns (boundary first) with their face slots; receive list ----
+  const bool wtile = PRESS && g.west_bc && ti == 0;
   const int ncol = TI * TJ;
-  const int nwork = ncol * KH;
-  const bool wphys = press && g.west_bc && ti == 0;
-  __shared__ double red[16];
+  const int nbnd = (TI <= 2 || TJ <= 2) ? ncol : 2 * TJ + 2 * (TI - 2);
+  for (int c = tid; c < ncol; c += nth) {
+    int li, lj;
+    if (nbnd == ncol) {
+      li = 1 + c / TJ;
+      lj = 1 + c % TJ;
+    } else if (c < TJ) {
+      li = 1; lj = 1 + c;
+    } else if (c < 2 * TJ) {
+      li = TI; lj = 1 + (c - TJ);
+    } else if (c < nbnd) {
+      const int r = c - 2 * TJ;
+      li = 2 + (r >> 1);
+      lj = (r & 1) ? TJ : 1;
+    } else {
+      const int r = c - nbnd;  // interior (li, lj) in [2, TI-1] x [2, TJ-1]
+      li = 2 + r / (TJ - 2);
+      lj = 2 + r % (TJ - 2);
+    }
+    const int i = I0 - 1 + li, j = J0 - 1 + lj;
+    coltab[c] = (unsigned)colbase(li, lj) | ((unsigned)((i + j) & 1) << 28) |
+                ((wtile && li == 1) ? (1u << 29) : 0u);
+    pubcol[c] = make_int4(li == 1 ? (int)(0 * fstride + (lj - 1) * KK) : -1,
+                          li == TI ? (int)(1 * fstride + (lj - 1) * KK) : -1,
+                          lj == 1 ? (int)(2 * fstride + (li - 1) * KK) : -1,
+                          lj == TJ ? (int)(3 * fstride + (li - 1) * KK) : -1);
+  }
+  const int nfc = 2 * TJ + 2 * TI;
+  for (int q = tid; q < nfc; q += nth) {
+    int f, m;
+    if (q < 2 * TJ) { f = q / TJ; m = q - f * TJ; }
+    else { f = 2 + (q - 2 * TJ) / TI; m = (q - 2 * TJ) - (f - 2) * TI; }
+    // receive: halo column on side f <- neighbour's face f^1
+    const int rli = f == 0 ? 0 : (f == 1 ? TI + 1 : 1 + m);
+    const int rlj = f == 2 ? 0 : (f == 3 ? TJ + 1 : 1 + m);
+    const bool wrap = (f == 2 && tj == 0) || (f == 3 && tj == pl.nj - 1);
+    // parity of the source column (the neighbour's cell, across the wrap for y)
+    const int si_ = I0 - 1 + rli, sj0 = J0 - 1 + rlj;
+    const int sj_ = sj0 == 0 ? g.jm : (sj0 == g.jm + 1 ? 1 : sj0);
+    rcvtab[q] = make_int4(colbase(rli, rlj), nbr[f] < 0 ? -1 : (int)(nbr[f] * tstride + (f ^ 1) * fstride + m * KK),
+                          wrap ? wrap_flip : 0, (si_ + sj_) & 1);
+  }
+
+  // ---- load tile columns, rhs and halo columns from global memory (warp per column) ----
+  const int ncol_h = (TI + 2) * (TJ + 2);
+  for (int col = warp; col < ncol_h; col += RES_WARPS) {
+    const int li = col / (TJ + 2), lj = col - li * (TJ + 2);
+    const bool ih = li == 0 || li == TI + 1, jh = lj == 0 || lj == TJ + 1;
+    if (ih && jh) continue;  // corner columns are never read
+    const int i = I0 - 1 + li, j = J0 - 1 + lj;
+    const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
+    const bool xphys = ih && (i == 0 || i == g.im + 1);
+    for (int k = lane; k <= km + 1; k += 32) {
+      const bool kh = k == 0 || k == km + 1;
+      float v;
+      if (!PRESS) {
+        v = a.p[cidx(g, i, j, k)];  // stored halo, or neighbour tile's initial value
+      } else if (kh || xphys) {
+        v = 0.0f;                   // top / east: 0; bottom / west: remapped at read time
+      } else {
+        v = a.p[cidx(g, i, jj, k)]; // periodic y halo: pre-pass snapshot of the source
+      }
+      const int slot = colbase(li, lj) + colour(i, j, k) * KK + (k >> 1);
+      S[slot] = v;
+      if (!ih && !jh && !kh) S[slot + 2 * KK] = a.rhs[cidx(g, i, j, k)];
+    }
+  }
+  __syncthreads();
+  // tags: pass n of this launch is tag0 + n + 2 (the initial publish below
+  // plays passes -2 and -1); *epoch advances by the tags a launch uses, so
+  // tags never repeat across launches and stale words can never match
+  const unsigned tag0 = 1u + *a.epoch;
+  // initial publish: both colours of the boundary columns, as passes -2
+  // (colour 0) and -1 (colour 1) of the ring of face buffers
+  for (int w = tid; w < nbnd * 2 * KK; w += nth) {
+    const int c = w / (2 * KK), r = w - c * 2 * KK;
+    const int col_c = r >= KK ? 1 : 0, sl = r - col_c * KK;
+    const int4 f = pubcol[c];
+    const float v = S[(coltab[c] & CB_MASK) + r];
+    unsigned long long* X = a.xbuf + (2 + col_c) * bstride + (long long)tile * tstride;
+    const unsigned tag = tag0 + (unsigned)col_c;
+    if (f.x >= 0) st_ll(X + f.x + sl, v, tag);
+    if (f.y >= 0) st_ll(X + f.y + sl, v, tag);
+    if (f.z >= 0) st_ll(X + f.z + sl, v, tag);
+    if (f.w >= 0) st_ll(X + f.w + sl, v, tag);
+  }
+
+  // runs: every thread gets about one boundary run and one interior run
+  const int nseg_b = max(1, min(KT, nbnd > 0 ? nth / nbnd : 1));
+  const int L_b = (KT + nseg_b - 1) / nseg_b;
+  const int nint = ncol - nbnd;
+  const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
+  const int L_i = (KT + nseg_i - 1) / nseg_i;
+  // receive walk over (face column q, slot sl)
+  const int nrcv = nfc * KK;
+  const int rq0 = tid / KK, rs0 = tid - rq0 * KK;
+  const int rdq = nth / KK, rdr = nth - rdq * KK;
+  bool timed_out = false;
 
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
-    float* Sc = S + nrd * csz;         // cells being updated
-    const float* So = S + (1 - nrd) * csz;  // their neighbours
-    const float* Rc = R + nrd * csz;
+    // Receive the neighbours' faces into this tile's colour-(1-nrd) halo
+    // slots: pass n-1's publish, or pass n-2's across an odd-jm periodic wrap.
+    // Those slots were last read in pass n-2, which every thread finished
+    // before the barrier of pass n-1, so no barrier is needed before this.
+    {
+      const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
+      const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
+      const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
+      float* Sd = S + (1 - nrd) * KK;
+      int q = rq0, sl = rs0;
+      for (int w0 = 0; w0 < ((a.debug & 4) ? 0 : nrcv); w0 += 4 * nth) {
+        const unsigned long long* src[4];
+        unsigned want[4];
+        int dst[4];
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dst[u] = -1;
+          if (q < nfc) {
+            const int4 e = rcvtab[q];
+            // only slots holding cells of the source colour were published
+            const int kps = (((1 - nrd) ^ e.z) + e.w + 1) & 1;
+            const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
+            if (e.y >= 0 && valid) {
+              src[u] = (e.z ? XB2 : XB1) + e.y + sl;
+              want[u] = e.z ? t2 : t1;
+              dst[u] = e.x + sl;
+              v[u] = ld_ll(src[u]);
+            }
+          }
+          sl += rdr;
+          q += rdq;
+          if (sl >= KK) {
+            sl -= KK;
+            ++q;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (dst[u] < 0) continue;
+          unsigned spins = 0;
+          while ((unsigned)(v[u] >> 32) != want[u] && !timed_out && !(a.debug & 1)) {
+            if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
+              atomicOr(a.err, 1u);
+              timed_out = true;
+            }
+            v[u] = ld_ll(src[u]);
+          }
+          Sd[dst[u]] = __uint_as_float((unsigned)v[u]);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
+    const unsigned tag = tag0 + (unsigned)(n + 2);
     double acc = 0.0;
-    for (int w = tid; w < nwork; w += nth) {
-      const int col = w / KH, t = w - col * KH;
-      const int li = 1 + col / TJ, lj = 1 + (col - (li - 1) * TJ);
-      const int i = I0 - 1 + li, j = J0 - 1 + lj;
-      const int k = 1 + ((i + j + nrd) & 1) + 2 * t;  // colour(i,j,k) == nrd
-      if (k > g.km) continue;
-      const int s = sidx(li, lj, k);
-      const int sk_lo = li * sI + lj * sJ + ((k - 1) >> 1);
-      const int sk_hi = li * sI + lj * sJ + ((k + 1) >> 1);
-      const float pc = Sc[s];
-      const float pE = So[s + sI];
-      const float pW = (wphys && li == 1) ? pc : So[s - sI];
-      const float pN = So[s + sJ];
-      const float pS = So[s - sJ];
-      const float pT = So[sk_hi];
-      const float pB = (press && k == 1) ? pc : So[sk_lo];
-      float nb = a.cf.cn2l[i - 1] * pE;
-      nb = nb + a.cf.cn2s[i - 1] * pW;
-      nb = nb + a.cf.cn3l[j - 1] * pN;
-      nb = nb + a.cf.cn3s[j - 1] * pS;
-      nb = nb + a.cf.cn4l[k - 1] * pT;
-      nb = nb + a.cf.cn4s[k - 1] * pB;
-      const float rel = a.om * (a.cf.cn1s * (nb - Rc[s]) - pc);
-      Sc[s] = pc + rel;
-      acc += (double)rel * (double)rel;
-    }
-    __syncthreads();
-    // publish this pass's colour on the 4 faces: [face][m][kk] with m along the face
-    float* X = a.xbuf + ((long long)(n & 1) * ntiles + tile) * 4 * fstride;
-    {
-      const int nf0 = TJ * KK, nf2 = TI * KK;
-      const int tot = 2 * nf0 + 2 * nf2;
-      for (int idx = tid; idx < tot; idx += nth) {
-        int f, m, kk;
-        if (idx < 2 * nf0) {
-          f = idx / nf0;
-          const int r = idx - f * nf0;
-          m = r / KK;
-          kk = r - m * KK;
-        } else {
-          const int r0 = idx - 2 * nf0;
-          f = 2 + r0 / nf2;
-          const int r = r0 - (f - 2) * nf2;
-          m = r / KK;
-          kk = r - m * KK;
-        }
-        const int li = f == 0 ? 1 : (f == 1 ? TI : 1 + m);
-        const int lj = f == 2 ? 1 : (f == 3 ? TJ : 1 + m);
-        __stcg(X + f * fstride + m * KK + kk, Sc[li * sI + lj * sJ + kk]);
-      }
-    }
-    const double bs = block_sum<16>(acc, red);
-    if (tid == 0) a.partials[(long long)n * ntiles + tile] = bs;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(a.flags + tile, (unsigned)(n + 1));
-    if (tid < 4 && nbr[tid] >= 0) {
-      const unsigned* fl = a.flags + nbr[tid];
-      unsigned spins = 0;
-      while (ld_acquire(fl) < (unsigned)(n + 1)) {
-        if (++spins > (1u << 26)) {  // ~seconds: never hang the GPU
-          atomicOr(a.err, 1u);
-          break;
-        }
-        if (spins > 64) __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    // receive: neighbour faces into this tile's halo slots
-    {
-      const int nf0 = TJ * KK, nf2 = TI * KK;
-      const int tot = 2 * nf0 + 2 * nf2;
-      for (int idx = tid; idx < tot; idx += nth) {
-        int side, m, kk;
-        if (idx < 2 * nf0) {
-          side = idx / nf0;
-          const int r = idx - side * nf0;
-          m = r / KK;
-          kk = r - m * KK;
-        } else {
-          const int r0 = idx - 2 * nf0;
-          side = 2 + r0 / nf2;
-          const int r = r0 - (side - 2) * nf2;
-          m = r / KK;
-          kk = r - m * KK;
-        }
-        const int src = nbr[side];
-        if (src < 0) continue;
-        // west reads the neighbour's east face (1), east its west face (0), ...
-        const int sface = side ^ 1;
-        const float* XS = a.xbuf + ((long long)(n & 1) * ntiles + src) * 4 * fstride + sface * fstride;
-        const int li = side == 0 ? 0 : (side == 1 ? TI + 1 : 1 + m);
-        const int lj = side == 2 ? 0 : (side == 3 ? TJ + 1 : 1 + m);
-        const bool wrap = (side == 2 && tj == 0) || (side == 3 && tj == pl.nj - 1);
-        const int slot_colour = nrd ^ (wrap ? wrap_flip : 0);
-        const float v = __ldcg(XS + m * KK + kk);
-        // only slots whose source cell has colour nrd changed in this pass
-        const int i = I0 - 1 + li, j = J0 - 1 + lj;
-        const int k_src_par = (i + j + 1 + slot_colour) & 1;  // k parity of slot-colour cells here
-        const int k = 2 * kk + k_src_par;
-        if (k < 1 || k > g.km) continue;
-        S[slot_colour * csz + li * sI + lj * sJ + kk] = v;
-      }
-    }
-    __syncthreads();
+    if (!(a.debug & 2)) acc = update_phase<PRESS, true>(a, S, coltab, pubcol, X, tag, 0, nbnd, nseg_b, L_b, KT, nrd, KK, CW,
+                                           sI, km);
+    if (!(a.debug & 2)) acc += update_phase<PRESS, false>(a, S, coltab, pubcol, X, tag, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW,
+                                      sI, km);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) a.partials[((long long)n * ntiles + tile) * RES_WARPS + warp] = acc;
   }
+  __syncthreads();
 
-  // ---- write the tile back ----
-  for (int idx = tid; idx < ncol * g.km; idx += nth) {
-    const int col = idx / g.km, k = 1 + (idx - col * g.km);
-    const int li = 1 + col / TJ, lj = 1 + (col - (li - 1) * TJ);
+  // ---- write the tile back (warp per column); press: closed-form halo ----
+  unsigned bad = 0;
+  for (int c = warp; c < ncol; c += RES_WARPS) {
+    const int li = 1 + c / TJ, lj = 1 + (c - (c / TJ) * TJ);
     const int i = I0 - 1 + li, j = J0 - 1 + lj;
-    a.p[cidx(g, i, j, k)] = S[colour(i, j, k) * csz + sidx(li, lj, k)];
+    const int cb = colbase(li, lj);
+    // targets: the column itself, plus the halo columns whose closed-form
+    // source is this column (les.py:341-355: k first, then j, then i)
+    int ti_[2] = {i, (PRESS && i == 1) ? 0 : -1};
+    int tj_[3] = {j, (PRESS && j == 1) ? g.jm + 1 : -1, (PRESS && j == g.jm) ? 0 : -1};
+    for (int k = lane; k <= km + 1; k += 32) {
+      const int kr = k == 0 ? 1 : (k > km ? km : k);
+      const float v = S[cb + colour(i, j, kr) * KK + (kr >> 1)];
+      const bool own = k >= 1 && k <= km;
+      if (own && !finite32(v)) bad = F_PRESS;
+      const float hv = (k == km + 1) ? 0.0f : v;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (ti_[x] < 0) continue;
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          if (tj_[y] < 0) continue;
+          const bool self = x == 0 && y == 0;
+          if (self && !own && !PRESS) continue;  // stored halo: untouched
+          a.p[cidx(g, ti_[x], tj_[y], k)] = self && own ? v : hv;
+        }
+      }
+      if (PRESS && i == g.im) {  // east face is Dirichlet 0 for every j' mapped here
+#pragma unroll
+        for (int y = 0; y < 3; ++y)
+          if (tj_[y] >= 0) a.p[cidx(g, g.im + 1, tj_[y], k)] = 0.0f;
+      }
+    }
+  }
+  if (a.pflags) flag_or(a.pflags, bad);
+
+  // ---- residuals: tile b sums iteration b over tiles and warps in a fixed order ----
+  cg::this_grid().sync();
+  if (tid == 0 && tile == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);  // fresh tags for the next launch
+  const int per_pass = ntiles * RES_WARPS;
+  for (int it = tile; it < a.n_iter; it += ntiles) {
+    double tot = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const double* q = a.partials + (long long)(2 * it + pass) * per_pass;
+      double v = 0.0;
+      for (int b = tid; b < per_pass; b += nth) v += q[b];
+      v = block_sum<RES_WARPS>(v, red);
+      __syncthreads();
+      tot += v;
+    }
+    if (tid == 0) a.res[it] = tot;
   }
 }
 
@@ -260,6 +454,14 @@ __global__ void __launch_bounds__(512, 1) k_sor_resident(ResArgs a) {
 // ---------------------------------------------------------------------------
 static int g_num_sms = -1;
 static int g_max_smem = -1;
+
+static size_t plan_smem(int tim, int tjm, int kk) {
+  const size_t arrays = 4ull * ((((size_t)4 * kk + 1) * (tim + 2) * (tjm + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
+  const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
+  const size_t pubcol = 16ull * tim * tjm;
+  const size_t rcvtab = 16ull * 2 * (tim + tjm);
+  return arrays + coltab + pubcol + rcvtab;
+}
 
 ResPlan plan_resident(const Geo& g, int device) {
   ResPlan pl{};
@@ -270,12 +472,12 @@ ResPlan plan_resident(const Geo& g, int device) {
   }
   if (g_num_sms <= 0 || !g.west_bc || !g.east_bc || g.ioff != 0) return pl;
   pl.kk = ((g.km + 1) >> 1) + 1;
-  pl.nthreads = 512;
+  pl.kt = (g.km + 1) >> 1;
   size_t best = (size_t)-1;
   for (int ni = 1; ni <= g.im && ni <= g_num_sms; ++ni) {
     for (int nj = 1; nj <= g.jm && ni * nj <= g_num_sms; ++nj) {
       const int tim = (g.im + ni - 1) / ni, tjm = (g.jm + nj - 1) / nj;
-      const size_t smem = 4 * (size_t)2 * 2 * (tim + 2) * (tjm + 2) * pl.kk;
+      const size_t smem = plan_smem(tim, tjm, pl.kk);
       if (smem > (size_t)g_max_smem - 2048) continue;
       // cost: largest tile's cells plus a face-exchange term
       const size_t cost = (size_t)tim * tjm * 4 + 2 * (size_t)(tim + tjm);
@@ -291,48 +493,78 @@ ResPlan plan_resident(const Geo& g, int device) {
   }
   if (best == (size_t)-1) return pl;
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
-  pl.xbuf = 2LL * pl.ni * pl.nj * 4 * fmax * pl.kk;
+  pl.xbuf = 4LL * pl.ni * pl.nj * 4 * fmax * pl.kk;
   pl.ok = true;
   return pl;
 }
 
 bool resident_supported(const Geo& g, const SorC& cf, int device) {
-  if (cf.cn1 != nullptr) return false;  // cn1 must be a scalar
-  return plan_resident(g, device).ok;
+  if (cf.cn1 != nullptr || !cf.uni) return false;  // scalar cn1 and neighbour weights
+  return plan_resident(g, device).ok || regrun_view(g, device).ok;
+}
+
+// The register-run kernel (sor_regrun.cu) is used when its plan fits (every
+// thread's run of cells in registers), else this generic one.
+static bool use_regrun(const Geo& g, int device) {
+  static const int force_generic = getenv("LESB_RESIDENT_GENERIC") ? atoi(getenv("LESB_RESIDENT_GENERIC")) : 0;
+  return !force_generic && regrun_view(g, device).ok;
 }
 
 int resident_ntiles(const Geo& g, int device) {
+  if (use_regrun(g, device)) return regrun_view(g, device).ntiles;
   ResPlan pl = plan_resident(g, device);
   return pl.ok ? pl.ni * pl.nj : 0;
 }
 
-long long resident_xbuf_floats(const Geo& g, int device) {
+int resident_partials(const Geo& g, int device) {
   ResPlan pl = plan_resident(g, device);
-  return pl.ok ? pl.xbuf : 0;
+  const int a = pl.ok ? pl.ni * pl.nj * RES_WARPS : 0;
+  const int b = regrun_view(g, device).partials;
+  return a > b ? a : b;
 }
 
-cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
-                                int n_iter, int policy, float* xbuf, unsigned* flags, double* partials,
-                                unsigned* err, cudaStream_t st) {
+long long resident_xbuf_words(const Geo& g, int device) {
   ResPlan pl = plan_resident(g, device);
-  if (!pl.ok) return cudaErrorInvalidValue;
-  static int attr_set = 0;
-  if (attr_set < (int)pl.smem) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_sor_resident);
-    if (e != cudaSuccess) return e;
-    const int dyn_max = g_max_smem - (int)fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(k_sor_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
-    if (e != cudaSuccess) return e;
-    attr_set = dyn_max;
-  }
-  const int ntiles = pl.ni * pl.nj;
-  cudaError_t e = cudaMemsetAsync(flags, 0, ntiles * sizeof(unsigned), st);
+  const long long a = pl.ok ? pl.xbuf : 0;
+  const long long b = regrun_view(g, device).xbuf;
+  return a > b ? a : b;
+}
+
+template <bool PRESS>
+static cudaError_t set_smem_attr(size_t smem) {
+  static size_t attr_set = 0;
+  if (attr_set >= smem) return cudaSuccess;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, k_sor_resident<PRESS>);
   if (e != cudaSuccess) return e;
-  ResArgs a{g, pl, p, rhs, cf, om, n_iter, policy, xbuf, flags, partials, err};
+  const int dyn_max = g_max_smem - (int)fa.sharedSizeBytes;
+  e = cudaFuncSetAttribute(k_sor_resident<PRESS>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+  if (e != cudaSuccess) return e;
+  attr_set = (size_t)dyn_max;
+  return cudaSuccess;
+}
+
+// One launch does the whole solve: n_iter iterations, the press halo (policy
+// 1) with its non-finite check into pflags, and res[n_iter].  xbuf holds
+// resident_xbuf_words() 64-bit words, zeroed once; *epoch starts at 0 and is
+// advanced by every launch (both are reset after a timeout).
+cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
+                                int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
+                                double* res, unsigned* pflags, unsigned* err, cudaStream_t st) {
+  if (use_regrun(g, device))
+    return launch_sor_regrun(g, device, p, rhs, cf, om, n_iter, policy, xbuf, epoch, partials, res, pflags, err, st);
+  ResPlan pl = plan_resident(g, device);
+  if (!pl.ok || !cf.uni || cf.cn1) return cudaErrorInvalidValue;
+  cudaError_t e = policy == 1 ? set_smem_attr<true>(pl.smem) : set_smem_attr<false>(pl.smem);
+  if (e != cudaSuccess) return e;
+  const int ntiles = pl.ni * pl.nj;
+  ResArgs a{g,      pl,     p,      rhs,  om,    cf.cn1s,  cf.w2l, cf.w2s, cf.w3l, cf.w3s,
+            cf.w4l, cf.w4s, n_iter, (unsigned long long*)xbuf, epoch, partials, res, pflags, err, 0};
+  static const int dbg = getenv("LESB_RES_DEBUG") ? atoi(getenv("LESB_RES_DEBUG")) : 0;
+  a.debug = dbg;
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((const void*)k_sor_resident, dim3(ntiles), dim3(pl.nthreads), args, pl.smem,
-                                     st);
+  const void* fn = policy == 1 ? (const void*)k_sor_resident<true> : (const void*)k_sor_resident<false>;
+  return cudaLaunchCooperativeKernel(fn, dim3(ntiles), dim3(RES_THREADS), args, pl.smem, st);
 }
 
 }  // namespace lesb

@@ -20,13 +20,14 @@ def current_device() -> int:
     return int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("LESB_USE_LOCAL_RANK") else 0
 
 
-SOR_AUTO, SOR_STREAMING, SOR_RESIDENT = 0, 1, 2
+SOR_AUTO, SOR_PASSES, SOR_RESIDENT, SOR_FUSED = 0, 1, 2, 3
 
 
 def set_sor_path(path: int) -> None:
     """Red-black solver implementation for new domains and the host-buffer
-    solver: 0 auto, 1 streaming colour passes, 2 shared-memory resident.
-    Results are bitwise identical; this only selects the kernels."""
+    solver: 0 auto, 1 unfused colour passes, 2 shared-memory resident,
+    3 colour-fused streaming.  Results are bitwise identical; this only
+    selects the kernels."""
     from . import _native as N
 
     N.check(N.load().lesb_set_default_sor_path(int(path)), "lesb_set_default_sor_path")

@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -15
+python scripts/prof_press.py --path 2
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sor_resident -s 1 -c 1 -o gpurun_out/prof_resident5 python scripts/prof_press.py --path 2 --reps 2 > gpurun_out/ncu_res5.log 2>&1

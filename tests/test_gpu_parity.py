@@ -21,11 +21,12 @@ FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p")
 RTOL_RES = 1e-12
 
 
-@pytest.fixture(scope="module", params=[1, 0], ids=["streaming", "resident"])
+@pytest.fixture(scope="module", params=[1, 0, 3], ids=["passes", "resident", "fused"])
 def P(request):
-    """The package with the red-black solver forced to the streaming kernels
-    (1) or left on auto, which selects the shared-memory-resident persistent
-    kernel wherever the grid fits (0).  Every test runs on both."""
+    """The package with the red-black solver forced to the unfused colour
+    passes (1), left on auto, which selects the shared-memory-resident
+    persistent kernel wherever the grid fits (0), or forced to the
+    colour-fused streaming kernel (3).  Every test runs on all three."""
     import paper_1504_02264_b200 as pkg
 
     pkg.runtime.set_sor_path(request.param)
@@ -267,6 +268,6 @@ def test_solver_path_selection(P):
     h = fs.handle()
     fs._ensure_coeffs(h)
     path = N.load().lesb_sor_path_in_use(h.h, 0)
-    assert path in (1, 2)
+    assert path in (1, 2, 3)
     lib = N.load()
     assert lib.lesb_sor_path_in_use(h.h, 1) == 1  # twinned always streams
