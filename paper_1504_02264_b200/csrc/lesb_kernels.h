@@ -85,16 +85,4 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
                                 int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
                                 double* res, unsigned* pflags, unsigned* err, cudaStream_t st);
 
-// sor_regrun.cu (register-run variant, chosen by launch_sor_resident when it fits)
-struct RRPlanView {
-  int ntiles;
-  long long xbuf;
-  int partials;  // per-pass residual partials
-  bool ok;
-};
-RRPlanView regrun_view(const Geo& g, int device);
-cudaError_t launch_sor_regrun(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
-                              int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials, double* res,
-                              unsigned* pflags, unsigned* err, cudaStream_t st);
-
 }  // namespace lesb

@@ -271,7 +271,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
                           wrap ? wrap_flip : 0, (si_ + sj_) & 1);
   }
 
-  // ---- load tile columns, rhs and halo columns from global memory (warp per column) ----
+  // ---- load tile columns, rhs and halo columns from global memory (warp per
+  // column).  Every element is an asynchronous 4-byte copy (cp.async, zero-fill
+  // where the value is a constant 0), so all of a thread's loads are in flight
+  // at once instead of one L2 round trip per column chunk. ----
+  const unsigned sm_s = (unsigned)__cvta_generic_to_shared(S);
   const int ncol_h = (TI + 2) * (TJ + 2);
   for (int col = warp; col < ncol_h; col += RES_WARPS) {
     const int li = col / (TJ + 2), lj = col - li * (TJ + 2);
@@ -280,22 +284,29 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     const int i = I0 - 1 + li, j = J0 - 1 + lj;
     const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
     const bool xphys = ih && (i == 0 || i == g.im + 1);
+    // stored halo / neighbour tile's initial value, or (press) the periodic y
+    // halo's pre-pass snapshot of its source
+    const float* src = a.p + cidx(g, i, PRESS ? jj : j, 0);
+    const float* rsrc = a.rhs + cidx(g, i, j, 0);
+    const bool inner = !ih && !jh;
+    const int cb = colbase(li, lj);
+    const int c0 = colour(i, j, 0);
     for (int k = lane; k <= km + 1; k += 32) {
       const bool kh = k == 0 || k == km + 1;
-      float v;
-      if (!PRESS) {
-        v = a.p[cidx(g, i, j, k)];  // stored halo, or neighbour tile's initial value
-      } else if (kh || xphys) {
-        v = 0.0f;                   // top / east: 0; bottom / west: remapped at read time
-      } else {
-        v = a.p[cidx(g, i, jj, k)]; // periodic y halo: pre-pass snapshot of the source
-      }
-      const int slot = colbase(li, lj) + colour(i, j, k) * KK + (k >> 1);
-      S[slot] = v;
-      if (!ih && !jh && !kh) S[slot + 2 * KK] = a.rhs[cidx(g, i, j, k)];
+      // press: top / east are 0; bottom / west are remapped at read time
+      const bool zero = PRESS && (kh || xphys);
+      const unsigned slot = (unsigned)(cb + (c0 ^ (k & 1)) * KK + (k >> 1));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sm_s + 4u * slot), "l"(src + k),
+                   "r"(zero ? 0u : 4u)
+                   : "memory");
+      if (inner && !kh)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sm_s + 4u * (slot + 2u * KK)), "l"(rsrc + k)
+                     : "memory");
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+
   // tags: pass n of this launch is tag0 + n + 2 (the initial publish below
   // plays passes -2 and -1); *epoch advances by the tags a launch uses, so
   // tags never repeat across launches and stale words can never match
@@ -500,34 +511,22 @@ ResPlan plan_resident(const Geo& g, int device) {
 
 bool resident_supported(const Geo& g, const SorC& cf, int device) {
   if (cf.cn1 != nullptr || !cf.uni) return false;  // scalar cn1 and neighbour weights
-  return plan_resident(g, device).ok || regrun_view(g, device).ok;
-}
-
-// The register-run kernel (sor_regrun.cu) is used when its plan fits (every
-// thread's run of cells in registers), else this generic one.
-static bool use_regrun(const Geo& g, int device) {
-  static const int force_generic = getenv("LESB_RESIDENT_GENERIC") ? atoi(getenv("LESB_RESIDENT_GENERIC")) : 0;
-  return !force_generic && regrun_view(g, device).ok;
+  return plan_resident(g, device).ok;
 }
 
 int resident_ntiles(const Geo& g, int device) {
-  if (use_regrun(g, device)) return regrun_view(g, device).ntiles;
   ResPlan pl = plan_resident(g, device);
   return pl.ok ? pl.ni * pl.nj : 0;
 }
 
 int resident_partials(const Geo& g, int device) {
   ResPlan pl = plan_resident(g, device);
-  const int a = pl.ok ? pl.ni * pl.nj * RES_WARPS : 0;
-  const int b = regrun_view(g, device).partials;
-  return a > b ? a : b;
+  return pl.ok ? pl.ni * pl.nj * RES_WARPS : 0;
 }
 
 long long resident_xbuf_words(const Geo& g, int device) {
   ResPlan pl = plan_resident(g, device);
-  const long long a = pl.ok ? pl.xbuf : 0;
-  const long long b = regrun_view(g, device).xbuf;
-  return a > b ? a : b;
+  return pl.ok ? pl.xbuf : 0;
 }
 
 template <bool PRESS>
@@ -551,8 +550,6 @@ static cudaError_t set_smem_attr(size_t smem) {
 cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
                                 int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
                                 double* res, unsigned* pflags, unsigned* err, cudaStream_t st) {
-  if (use_regrun(g, device))
-    return launch_sor_regrun(g, device, p, rhs, cf, om, n_iter, policy, xbuf, epoch, partials, res, pflags, err, st);
   ResPlan pl = plan_resident(g, device);
   if (!pl.ok || !cf.uni || cf.cn1) return cudaErrorInvalidValue;
   cudaError_t e = policy == 1 ? set_smem_attr<true>(pl.smem) : set_smem_attr<false>(pl.smem);
