@@ -6,6 +6,7 @@
 // coefficients.  One time step is captured once into a CUDA graph per
 // (n_iter, scheme, omega) and replayed.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -118,7 +119,8 @@ struct lesb_domain {
   long long n_py = 0;     // (im+2)*si : the Python-visible array
   std::mutex mu;
 
-  Spac spac() const { return Spac{dx1, dy1, dzn}; }
+  Spac sp{};  // spacings + exact reciprocals (set_spacing_info)
+  Spac spac() const { return sp; }
   SorC sorc() const {
     return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5], cuni, cw[0], cw[1], cw[2], cw[3], cw[4], cw[5]};
   }
@@ -131,6 +133,41 @@ struct lesb_domain {
 };
 
 namespace {
+
+// x is a power of two (normal, positive): its reciprocal is exact.
+bool pow2(float x) {
+  if (!(x > 0.0f) || !std::isfinite(x)) return false;
+  int e;
+  const float m = std::frexp(x, &e);
+  return m == 0.5f && x >= 1e-30f && x <= 1e30f;
+}
+
+// All n entries equal one power of two.
+bool uniform_pow2(const float* a, int n, float* h) {
+  for (int i = 1; i < n; ++i)
+    if (a[i] != a[0]) return false;
+  *h = a[0];
+  return pow2(a[0]);
+}
+
+// Record the exact-reciprocal information of the spacings and dt (Spac).
+void set_spacing_info(lesb_domain* h, const float* dx, const float* dy, const float* dz) {
+  Spac& s = h->sp;
+  s.dx1 = h->dx1;
+  s.dy1 = h->dy1;
+  s.dzn = h->dzn;
+  float hx = 0, hy = 0, hz = 0;
+  s.p2 = uniform_pow2(dx, h->g.im + 3, &hx) && uniform_pow2(dy, h->g.jm + 2, &hy) &&
+         uniform_pow2(dz, h->g.km + 2, &hz);
+  const float hs[3] = {hx, hy, hz};
+  for (int a = 0; a < 3; ++a) {
+    s.r1[a] = s.p2 ? 1.0f / hs[a] : 0.f;
+    s.r2[a] = s.p2 ? 1.0f / (hs[a] + hs[a]) : 0.f;
+    s.rsq[a] = s.p2 ? 1.0f / (hs[a] * hs[a]) : 0.f;
+  }
+  s.dtp2 = pow2(h->dt);
+  s.rdt = s.dtp2 ? 1.0f / h->dt : 0.f;
+}
 
 int ensure_partials(lesb_domain* h, int n_iter) {
   long long need = (long long)n_iter * 2 *
@@ -380,6 +417,7 @@ int lesb_create(const lesb_desc* d, lesb_handle* out) {
     if (err == cudaSuccess)
       err = cudaMemcpy(h->csd2, d->csd2, h->n_int() * sizeof(float), cudaMemcpyHostToDevice);
   }
+  if (err == cudaSuccess) set_spacing_info(h, d->dx1, d->dy1, d->dzn);
   if (err != cudaSuccess) {
     std::string m = std::string("lesb_create: ") + cudaGetErrorString(err);
     lesb_destroy(h);
@@ -458,6 +496,8 @@ int lesb_set_physics(lesb_handle h, float dt, float vn, float cs, const float* c
   h->vn = vn;
   h->cs = cs;
   h->csd2s = csd2_scalar;
+  h->sp.dtp2 = pow2(dt);
+  h->sp.rdt = h->sp.dtp2 ? 1.0f / dt : 0.f;
   if (csd2) {
     if (!h->csd2) CK(cudaMalloc(&h->csd2, h->n_int() * sizeof(float)));
     CK(cudaMemcpy(h->csd2, csd2, h->n_int() * sizeof(float), cudaMemcpyHostToDevice));

@@ -34,6 +34,15 @@ struct Spac {
   const float* dx1;  // im + 3
   const float* dy1;  // jm + 2
   const float* dzn;  // km + 2
+  // p2 != 0: every spacing of each axis equals one power of two h_a.  Every
+  // divisor on the path is then a power of two (h, 2h, h*h, and dt when
+  // dtp2), and x / 2^n == x * 2^-n exactly (both are the correctly rounded
+  // value of the same real number), so the kernels multiply by these exact
+  // reciprocals instead of dividing: bitwise identical, far fewer instructions.
+  int p2;
+  float r1[3], r2[3], rsq[3];  // 1/h, 1/(2h), 1/(h*h) per axis
+  int dtp2;
+  float rdt;                   // 1/dt
 };
 
 struct SorC {

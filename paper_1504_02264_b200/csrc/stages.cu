@@ -18,19 +18,25 @@ namespace lesb {
 // ---------------------------------------------------------------------------
 // velnw point updates (les.py:226-241):  f + dt*(fgh_a - ((p[+a]-p)*2)/(s[n]+s[n+1]))
 // ---------------------------------------------------------------------------
+template <bool P2 = false>
 __device__ __forceinline__ float velnw_u(const Geo& g, const Spac& s, const float* u, const float* p,
                                          const float* fgh, float dt, long long c, int i) {
-  float gx = ((p[c + g.si] - p[c]) * 2.0f) / (s.dx1[i] + s.dx1[i + 1]);
+  const float num = (p[c + g.si] - p[c]) * 2.0f;
+  const float gx = P2 ? num * s.r2[0] : num / (s.dx1[i] + s.dx1[i + 1]);
   return u[c] + dt * (fgh[3 * c + 0] - gx);
 }
+template <bool P2 = false>
 __device__ __forceinline__ float velnw_v(const Geo& g, const Spac& s, const float* v, const float* p,
                                          const float* fgh, float dt, long long c, int j) {
-  float gy = ((p[c + g.sj] - p[c]) * 2.0f) / (s.dy1[j] + s.dy1[j + 1]);
+  const float num = (p[c + g.sj] - p[c]) * 2.0f;
+  const float gy = P2 ? num * s.r2[1] : num / (s.dy1[j] + s.dy1[j + 1]);
   return v[c] + dt * (fgh[3 * c + 1] - gy);
 }
+template <bool P2 = false>
 __device__ __forceinline__ float velnw_w(const Geo& g, const Spac& s, const float* w, const float* p,
                                          const float* fgh, float dt, long long c, int k) {
-  float gz = ((p[c + 1] - p[c]) * 2.0f) / (s.dzn[k] + s.dzn[k + 1]);
+  const float num = (p[c + 1] - p[c]) * 2.0f;
+  const float gz = P2 ? num * s.r2[2] : num / (s.dzn[k] + s.dzn[k + 1]);
   return w[c] + dt * (fgh[3 * c + 2] - gz);
 }
 
@@ -102,6 +108,7 @@ __global__ void k_bondv1_inplace(Geo g, float* __restrict__ u, float* __restrict
 }
 
 // Fused velnw + bondv1 over the whole array: reads state A, writes B.
+template <bool P2>
 __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const float* __restrict__ v,
                                const float* __restrict__ w, const float* __restrict__ p,
                                const float* __restrict__ fgh, float dt, const float* __restrict__ inflow,
@@ -115,17 +122,17 @@ __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const
     long long c = cidx(g, i, j, k);
     bool interior = i >= 1 && i <= g.im && j >= 1 && j <= g.jm && k >= 1 && k <= g.km;
     if (interior) {
-      float a = velnw_u(g, s, u, p, fgh, dt, c, i);
-      float b = velnw_v(g, s, v, p, fgh, dt, c, j);
-      float d = velnw_w(g, s, w, p, fgh, dt, c, k);
+      float a = velnw_u<P2>(g, s, u, p, fgh, dt, c, i);
+      float b = velnw_v<P2>(g, s, v, p, fgh, dt, c, j);
+      float d = velnw_w<P2>(g, s, w, p, fgh, dt, c, k);
       if (!(finite32(a) && finite32(b) && finite32(d))) bits |= F_VELNW;
       ub[c] = a; vb[c] = b; wb[c] = d;
     } else {
       // velnw's own writes to halo faces are overwritten by bondv1 but are
       // still checked after the velnw stage (les.py:413-415).
-      if (in_velnw_u(g, i, j, k) && !finite32(velnw_u(g, s, u, p, fgh, dt, c, i))) bits |= F_VELNW;
-      if (in_velnw_v(g, i, j, k) && !finite32(velnw_v(g, s, v, p, fgh, dt, c, j))) bits |= F_VELNW;
-      if (in_velnw_w(g, i, j, k) && !finite32(velnw_w(g, s, w, p, fgh, dt, c, k))) bits |= F_VELNW;
+      if (in_velnw_u(g, i, j, k) && !finite32(velnw_u<P2>(g, s, u, p, fgh, dt, c, i))) bits |= F_VELNW;
+      if (in_velnw_v(g, i, j, k) && !finite32(velnw_v<P2>(g, s, v, p, fgh, dt, c, j))) bits |= F_VELNW;
+      if (in_velnw_w(g, i, j, k) && !finite32(velnw_w<P2>(g, s, w, p, fgh, dt, c, k))) bits |= F_VELNW;
       float* out[3] = {ub, vb, wb};
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
@@ -140,9 +147,9 @@ __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const
           int si_ = (int)(b.src / g.si);
           int sj_ = (int)((b.src % g.si) / g.sj);
           int sk_ = (int)(b.src % g.sj);
-          val = m == 0 ? velnw_u(g, s, u, p, fgh, dt, b.src, si_)
-              : (m == 1 ? velnw_v(g, s, v, p, fgh, dt, b.src, sj_)
-                        : velnw_w(g, s, w, p, fgh, dt, b.src, sk_));
+          val = m == 0 ? velnw_u<P2>(g, s, u, p, fgh, dt, b.src, si_)
+              : (m == 1 ? velnw_v<P2>(g, s, v, p, fgh, dt, b.src, sj_)
+                        : velnw_w<P2>(g, s, w, p, fgh, dt, b.src, sk_));
         }
         if (!finite32(val)) bits |= F_BONDV1;
         out[m][c] = val;
@@ -155,7 +162,7 @@ __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const
 // ---------------------------------------------------------------------------
 // velfg (les.py:90-192, _combine_force 128-175).  Component M at interior P.
 // ---------------------------------------------------------------------------
-template <int M>
+template <int M, bool P2 = false>
 __device__ __forceinline__ float velfg_point(const Geo& g, const Spac& s, const float* __restrict__ u,
                                              const float* __restrict__ v, const float* __restrict__ w,
                                              float vn, long long c, int i, int j, int k) {
@@ -170,20 +177,28 @@ __device__ __forceinline__ float velfg_point(const Geo& g, const Spac& s, const 
     const float* sa = d == 0 ? s.dx1 : (d == 1 ? s.dy1 : s.dzn);
     const float lo = sa[pd], hi = sa[pd + 1];
     // D_d(v_m, P): central (les.py:100-110)
-    const float d0 = (vm[c + sd] - vm[c - sd]) / (lo + hi);
+    const float n0 = vm[c + sd] - vm[c - sd];
+    const float d0 = P2 ? n0 * s.r2[d] : n0 / (lo + hi);
     // D_d(v_m, P + e_d): central, or one-sided at the global index N+1 (111-117)
     float d1;
     const bool onesided = (pd + 1 > nd) && (d != 0 || g.east_bc);
-    if (onesided) d1 = (vm[c + sd] - vm[c]) / sa[nd + 1];
-    else d1 = (vm[c + 2 * sd] - vm[c]) / (hi + sa[pd + 2]);
+    if (onesided) {
+      const float n1 = vm[c + sd] - vm[c];
+      d1 = P2 ? n1 * s.r1[d] : n1 / sa[nd + 1];
+    } else {
+      const float n1 = vm[c + 2 * sd] - vm[c];
+      d1 = P2 ? n1 * s.r2[d] : n1 / (hi + sa[pd + 2]);
+    }
     const float cov = V[d][c] * d0;
     const float cp = V[d][c + sd] * d1;
     if (d == M) {
-      avg[d] = (hi * cov + lo * cp) / (lo + hi);
-      term[d] = (2.0f * (-d0 + d1)) / (lo + hi);
+      const float na = hi * cov + lo * cp, nt = 2.0f * (-d0 + d1);
+      avg[d] = P2 ? na * s.r2[d] : na / (lo + hi);
+      term[d] = P2 ? nt * s.r2[d] : nt / (lo + hi);
     } else {
-      avg[d] = (cov + cp) / 2.0f;
-      term[d] = (-d0 + d1) / lo;
+      avg[d] = (cov + cp) * 0.5f;  // x / 2 == x * 0.5 exactly
+      const float nt = -d0 + d1;
+      term[d] = P2 ? nt * s.r1[d] : nt / lo;
     }
   }
   const float df = (term[0] + term[1]) + term[2];
@@ -249,7 +264,7 @@ struct MaskedReader {
   }
 };
 
-template <class R>
+template <class R, bool P2 = false>
 __device__ __forceinline__ void les_point(const Geo& g, const Spac& s, const R& rd, float csd2, long long c,
                                           int i, int j, int k, float lap_out[3]) {
   // neighbour reads: (m, axis, +/-).  on_axis_halo marks a j or k halo cell.
@@ -270,7 +285,10 @@ __device__ __forceinline__ void les_point(const Geo& g, const Spac& s, const R& 
 #pragma unroll
   for (int m = 0; m < 3; ++m)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) d[m][a] = (nb_hi[m][a] - nb_lo[m][a]) / den[a];
+    for (int a = 0; a < 3; ++a) {
+      const float nd_ = nb_hi[m][a] - nb_lo[m][a];
+      d[m][a] = P2 ? nd_ * s.r2[a] : nd_ / den[a];
+    }
   const float s11 = d[0][0], s22 = d[1][1], s33 = d[2][2];
   const float s12 = 0.5f * (d[0][1] + d[1][0]);
   const float s13 = 0.5f * (d[0][2] + d[2][0]);
@@ -282,7 +300,10 @@ __device__ __forceinline__ void les_point(const Geo& g, const Spac& s, const R& 
   for (int m = 0; m < 3; ++m) {
     float lap = 0.0f;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) lap = lap + ((nb_hi[m][a] - 2.0f * ctr[m]) + nb_lo[m][a]) / hh[a];
+    for (int a = 0; a < 3; ++a) {
+      const float nl = (nb_hi[m][a] - 2.0f * ctr[m]) + nb_lo[m][a];
+      lap = lap + (P2 ? nl * s.rsq[a] : nl / hh[a]);
+    }
     lap_out[m] = nu * lap;
   }
 }
@@ -344,8 +365,10 @@ __global__ void k_adam(float* __restrict__ fgh, float* __restrict__ fgh_old, lon
 // ---------------------------------------------------------------------------
 // divergence (les.py:330-338); rhs = divergence / dt (les.py:374-375)
 // ---------------------------------------------------------------------------
+template <bool P2 = false>
 __device__ __forceinline__ float div_point(const Geo& g, const Spac& s, float uc, float um, float vc, float vm,
                                            float wc, float wm, int i, int j, int k) {
+  if (P2) return ((uc - um) * s.r1[0] + (vc - vm) * s.r1[1]) + (wc - wm) * s.r1[2];
   return ((uc - um) / s.dx1[i] + (vc - vm) / s.dy1[j]) + (wc - wm) / s.dzn[k];
 }
 
@@ -366,6 +389,7 @@ __global__ void k_divergence(Geo g, Spac s, const float* __restrict__ u, const f
 // Reads the post-bondv1 velocities B; writes masked velocities to A, fgh,
 // fgh_old (interior: full chain; halo: adam only), and rhs (interior).
 // ---------------------------------------------------------------------------
+template <bool P2>
 __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const float* __restrict__ vb,
                             const float* __restrict__ wb, const float* __restrict__ mask,
                             float* __restrict__ fgh, float* __restrict__ fgh_old, float* __restrict__ ua,
@@ -381,13 +405,13 @@ __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const f
     bool interior = i >= 1 && i <= g.im && j >= 1 && j <= g.jm && k >= 1 && k <= g.km;
     if (interior) {
       float f[3];
-      f[0] = velfg_point<0>(g, s, ub, vb, wb, vn, c, i, j, k);
-      f[1] = velfg_point<1>(g, s, ub, vb, wb, vn, c, i, j, k);
-      f[2] = velfg_point<2>(g, s, ub, vb, wb, vn, c, i, j, k);
+      f[0] = velfg_point<0, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
+      f[1] = velfg_point<1, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
+      f[2] = velfg_point<2, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       if (!(finite32(f[0]) && finite32(f[1]) && finite32(f[2]))) bits |= F_VELFG;
       // feedbf
       const float m = mask[c];
-      const float coef = m / dt;
+      const float coef = (P2 && s.dtp2) ? m * s.rdt : m / dt;
       const float keep = 1.0f - m;
       const float vel[3] = {ub[c], vb[c], wb[c]};
       float vk[3];
@@ -403,7 +427,7 @@ __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const f
       MaskedReader rd{{ub, vb, wb}, mask, g};
       if (do_les) {
         float add[3];
-        les_point(g, s, rd, csd2f ? csd2f[icompact(g, i, j, k)] : csd2s, c, i, j, k, add);
+        les_point<MaskedReader, P2>(g, s, rd, csd2f ? csd2f[icompact(g, i, j, k)] : csd2s, c, i, j, k, add);
 #pragma unroll
         for (int a = 0; a < 3; ++a) f[a] = f[a] + add[a];
         if (!(finite32(f[0]) && finite32(f[1]) && finite32(f[2]))) bits |= F_LES;
@@ -425,7 +449,8 @@ __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const f
       const float um = rd(0, c - g.si, i - 1, 0);
       const float vm_ = rd(1, c - g.sj, i, j - 1 < 1);
       const float wm = rd(2, c - 1, i, k - 1 < 1);
-      rhs[c] = div_point(g, s, vk[0], um, vk[1], vm_, vk[2], wm, i, j, k) / dt;
+      const float dv = div_point<P2>(g, s, vk[0], um, vk[1], vm_, vk[2], wm, i, j, k);
+      rhs[c] = (P2 && s.dtp2) ? dv * s.rdt : dv / dt;
     } else if (i <= g.im + 1) {
       ua[c] = ub[c]; va[c] = vb[c]; wa[c] = wb[c];
 #pragma unroll
@@ -481,7 +506,8 @@ void launch_velnw_bondv1(const Geo& g, const Spac& s, const float* u, const floa
                          float* wb, unsigned* flags, cudaStream_t st) {
   dim3 gr, bl;
   box_launch(g.km + 2, g.jm + 2, g.im + 2, gr, bl);
-  k_velnw_bondv1<<<gr, bl, 0, st>>>(g, s, u, v, w, p, fgh, dt, inflow, ub, vb, wb, flags);
+  if (s.p2) k_velnw_bondv1<true><<<gr, bl, 0, st>>>(g, s, u, v, w, p, fgh, dt, inflow, ub, vb, wb, flags);
+  else k_velnw_bondv1<false><<<gr, bl, 0, st>>>(g, s, u, v, w, p, fgh, dt, inflow, ub, vb, wb, flags);
 }
 
 void launch_velfg(const Geo& g, const Spac& s, const float* u, const float* v, const float* w, float* fgh,
@@ -532,8 +558,12 @@ void launch_fused_rhs(const Geo& g, const Spac& s, const float* ub, const float*
                       cudaStream_t st) {
   dim3 gr, bl;
   box_launch(g.km + 2, g.jm + 2, g.im + 2, gr, bl);
-  k_fused_rhs<<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les, csd2f,
-                                 csd2s, flags);
+  if (s.p2)
+    k_fused_rhs<true><<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
+                                         csd2f, csd2s, flags);
+  else
+    k_fused_rhs<false><<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
+                                          csd2f, csd2s, flags);
 }
 
 void launch_check_finite(const float* a, long long n, unsigned* flags, unsigned bit, cudaStream_t st) {
