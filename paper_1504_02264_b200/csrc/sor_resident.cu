@@ -51,6 +51,7 @@ namespace lesb {
 
 constexpr int RES_THREADS = 512;
 constexpr int RES_WARPS = RES_THREADS / 32;
+constexpr int RCVB = 6;  // face values each thread has in flight while receiving
 
 struct ResPlan {
   int ni, nj;       // tile grid
@@ -77,6 +78,7 @@ struct ResArgs {
   unsigned* pflags;  // stage flag word (F_PRESS) or nullptr
   unsigned* err;     // set when a neighbour wait times out
   int debug;         // timing experiments only (LESB_RES_DEBUG): 1 no waits, 2 no updates, 4 no receive
+  unsigned long long* trace;  // LESB_RES_TRACE: [ntiles][2 n_iter][4] %globaltimer stamps, or nullptr
 };
 
 // Face exchange in the "LL" style: every published value travels with the
@@ -91,6 +93,12 @@ __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a)
   unsigned long long w;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a) : "memory");
   return w;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
@@ -169,7 +177,10 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
 }
 
 // All runs of this thread in columns [c0, c1): the columns are cut into nseg
-// runs of L cells and run u = (c - c0) * nseg + g goes to thread u % nth.
+// runs of L cells and run u = g * (c1 - c0) + (c - c0) goes to thread
+// u % nth.  Column-fastest numbering puts a warp's lanes in consecutive
+// columns at the same slot offset; with the odd column stride their shared
+// addresses fall in distinct banks.
 template <bool PRESS, bool PUBLISH>
 __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
                                                const int4* __restrict__ pubcol, unsigned long long* X,
@@ -177,8 +188,9 @@ __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const
                                                int KK, int CW, int sI, int km) {
   double acc = 0.0;
   const int nunits = (c1 - c0) * nseg;
+  const int ncc = c1 - c0;
   for (int u = threadIdx.x; u < nunits; u += RES_THREADS) {
-    const int cc = u / nseg, g = u - cc * nseg;
+    const int g = u / ncc, cc = u - g * ncc;
     const int c = c0 + cc;
     const int t0 = g * L;
     const int t1 = min(t0 + L, KT);
@@ -338,8 +350,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   const int rdq = nth / KK, rdr = nth - rdq * KK;
   bool timed_out = false;
 
+  unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * 4 : nullptr;
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
+    if (tr && tid == 0) tr[4 * n + 0] = gtimer();
     // Receive the neighbours' faces into this tile's colour-(1-nrd) halo
     // slots: pass n-1's publish, or pass n-2's across an odd-jm periodic wrap.
     // Those slots were last read in pass n-2, which every thread finished
@@ -350,13 +364,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
       float* Sd = S + (1 - nrd) * KK;
       int q = rq0, sl = rs0;
-      for (int w0 = 0; w0 < ((a.debug & 4) ? 0 : nrcv); w0 += 4 * nth) {
-        const unsigned long long* src[4];
-        unsigned want[4];
-        int dst[4];
-        unsigned long long v[4];
+      for (int w0 = 0; w0 < ((a.debug & 4) ? 0 : nrcv); w0 += RCVB * nth) {
+        const unsigned long long* src[RCVB];
+        unsigned want[RCVB];
+        int dst[RCVB];
+        unsigned long long v[RCVB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RCVB; ++u) {
           dst[u] = -1;
           if (q < nfc) {
             const int4 e = rcvtab[q];
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RCVB; ++u) {
           if (dst[u] < 0) continue;
           unsigned spins = 0;
           while ((unsigned)(v[u] >> 32) != want[u] && !timed_out && !(a.debug & 1)) {
@@ -393,13 +407,16 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
       }
     }
     __syncthreads();
+    if (tr && tid == 0) tr[4 * n + 1] = gtimer();
     unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)(n + 2);
     double acc = 0.0;
     if (!(a.debug & 2)) acc = update_phase<PRESS, true>(a, S, coltab, pubcol, X, tag, 0, nbnd, nseg_b, L_b, KT, nrd, KK, CW,
                                            sI, km);
+    if (tr && tid == 0) tr[4 * n + 2] = gtimer();
     if (!(a.debug & 2)) acc += update_phase<PRESS, false>(a, S, coltab, pubcol, X, tag, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW,
                                       sI, km);
+    if (tr && tid == 0) tr[4 * n + 3] = gtimer();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
     if (lane == 0) a.partials[((long long)n * ntiles + tile) * RES_WARPS + warp] = acc;
@@ -529,6 +546,9 @@ long long resident_xbuf_words(const Geo& g, int device) {
   return pl.ok ? pl.xbuf : 0;
 }
 
+static unsigned long long* g_tbuf = nullptr;  // LESB_RES_TRACE stamps of the last launch
+static size_t g_tcap = 0, g_tlen = 0;
+
 template <bool PRESS>
 static cudaError_t set_smem_attr(size_t smem) {
   static size_t attr_set = 0;
@@ -559,9 +579,33 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
             cf.w4l, cf.w4s, n_iter, (unsigned long long*)xbuf, epoch, partials, res, pflags, err, 0};
   static const int dbg = getenv("LESB_RES_DEBUG") ? atoi(getenv("LESB_RES_DEBUG")) : 0;
   a.debug = dbg;
+  a.trace = nullptr;
+  static const bool trace = getenv("LESB_RES_TRACE") != nullptr;
+  const size_t tneed = (size_t)ntiles * 2 * n_iter * 4;
+  if (trace) {
+    if (g_tcap < tneed) {
+      if (g_tbuf) cudaFree(g_tbuf);
+      cudaMalloc(&g_tbuf, tneed * 8);
+      g_tcap = tneed;
+    }
+    g_tlen = tneed;
+    a.trace = g_tbuf;
+  }
   void* args[] = {&a};
   const void* fn = policy == 1 ? (const void*)k_sor_resident<true> : (const void*)k_sor_resident<false>;
   return cudaLaunchCooperativeKernel(fn, dim3(ntiles), dim3(RES_THREADS), args, pl.smem, st);
 }
 
 }  // namespace lesb
+
+// Debug only (not in the public header): copy the last traced launch's
+// stamps ([tile][pass][4]: before receive, after receive barrier, after
+// boundary runs, after interior runs) to host; returns the word count.
+extern "C" long long lesb_debug_resident_trace(unsigned long long* host, long long cap) {
+  using namespace lesb;
+  if (!g_tbuf || !host) return 0;
+  const long long n = (long long)g_tlen < cap ? (long long)g_tlen : cap;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_tbuf, n * 8, cudaMemcpyDeviceToHost);
+  return n;
+}
