@@ -50,8 +50,8 @@ METRIC = "LES time steps/sec and MLUPS at 1/2/4/8 B200; % of HBM-bandwidth roofl
 IM, JM, KM = 150, 150, 90
 N_ITER = 50
 REINIT = 8
-B_STEP = 216 + 16 * N_ITER      # algorithmic bytes / interior cell / step (SURVEY 8(d))
-B_PASS_SCALAR_CN1 = 6           # one RB colour pass, cn1 scalar: (4 p r/w + 4 rhs) / 2 ... see DESIGN.md
+B_STEP = 216 + 16 * N_ITER      # algorithmic bytes / interior cell / step (SURVEY 8(d), BASELINE.md 4)
+B_ITER = 12                     # SOR RB iteration, cn1 a scalar: p read + p write + rhs read
 WORKLOAD = "config2: 150x150x90, h=2, dt=0.5, 3x3 buildings, log-law inflow, RB SOR 50 iters"
 
 
@@ -208,7 +208,8 @@ def run_gpu(args):
     stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0) + 1  # + async bookkeeping kernel
-    sor_path = {1: "streaming colour passes", 2: "shared-memory-resident persistent kernel"}[
+    sor_path = {1: "unfused colour passes", 2: "shared-memory-resident persistent kernel",
+                3: "colour-fused streaming iterations"}[
         lib.lesb_sor_path_in_use(hw.h, 0)]
 
     def reinit():
@@ -268,10 +269,20 @@ def run_gpu(args):
     n_int = IM * JM * KM
     hbm, peak_kind = peaks()
     phase_ms /= args.steps
-    sor_pass_ms = phase_ms[2] / (2 * N_ITER)
-    b_pass = 6 * n_int  # see DESIGN.md "algorithmic bytes": RB pass, scalar cn1
-    achieved = b_pass / (sor_pass_ms * 1e-3) / 1e9
+    # dominant kernel: the SOR solve (phase 2 = the solver launches between the
+    # step's fused kernel and the press halo).  Algorithmic bytes: 12 B per
+    # interior cell and iteration (SURVEY 8(d), cn1 scalar) x N x n_iter.
+    sor_ms = phase_ms[2]
+    b_solve = B_ITER * n_int * N_ITER
+    achieved = b_solve / (sor_ms * 1e-3) / 1e9
     step_gbs = B_STEP * n_int / (ms_per_step * 1e-3) / 1e9
+    sor_kernel = {2: "k_sor_resident", 3: "k_sor_rbfused", 1: "k_sor_rb"}[lib.lesb_sor_path_in_use(hw.h, 0)]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{sor_kernel}@{IM}x{JM}x{KM}")
+    except Exception:  # noqa: BLE001
+        traffic = None
 
     # ---- e2e through the public API ----
     e2e = (e2e_run(P, N, gi, torch, grid, st0, inflow, args) if not args.no_e2e
@@ -302,10 +313,13 @@ def run_gpu(args):
                               "frac": step_gbs / hbm, "peak_kind": peak_kind},
             "phase_ms": {"velnw_bondv1": phase_ms[0], "velfg_feedbf_les_adam_rhs": phase_ms[1],
                          "sor_passes": phase_ms[2], "halo_and_residuals": phase_ms[3]},
-            "roofline": {"kernel": "k_sor_rb (one red-black colour pass)", "bound": "hbm",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": b_pass, "launch_ms": sor_pass_ms},
+            "roofline": {"kernel": f"{sor_kernel} (whole {N_ITER}-iteration red-black solve, one launch)",
+                         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": b_solve, "bytes_per_cell_iteration": B_ITER,
+                         "launch_ms": sor_ms,
+                         "note": "working set (p, rhs: 17 MB) is L2/shared-memory resident at this size; "
+                                 "the HBM-bound evidence is the 512x512x90 press-only line (DESIGN.md)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e["value"], "unit": "steps/s", "h2d_bytes_per_step": e2e["h2d"],
                     "d2h_bytes_per_step": e2e["d2h"]},

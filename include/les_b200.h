@@ -117,6 +117,12 @@ int lesb_divergence(lesb_handle h, float* out_host);                /* les.py:33
 int lesb_strain_magnitude(lesb_handle h, float* out_host);          /* les.py:285-296, (im,jm,km) */
 int lesb_press(lesb_handle h, int n_iter, int scheme, float omega,
                double* residuals_out);                              /* les.py:358-381 */
+/* solve_pressure on the domain's device-resident p (in place) and rhs (set
+ * with lesb_upload(LESB_RHS)): the sor-bench path (cli.py:222-283,
+ * sor.py:255-309) without host copies.  halo_policy LESB_HALO_STORED or
+ * LESB_HALO_PRESS; residuals_out (host, n_iter doubles) may be NULL. */
+int lesb_sor_solve(lesb_handle h, int n_iter, int scheme, float omega, int halo_policy,
+                   double* residuals_out);
 
 /* ---- the time step (les.py:393-416) ---- */
 /* One step, synchronous: inflow (3 x km floats, host) in, residuals

@@ -644,6 +644,29 @@ int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* resid
   return LESB_OK;
 }
 
+int lesb_sor_solve(lesb_handle h, int n_iter, int scheme, float omega, int halo_policy, double* residuals_out) {
+  int rc = check_args_step(h, n_iter, scheme);
+  if (rc) return rc;
+  if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  rc = ensure_partials(h, n_iter);
+  if (rc) return rc;
+  if (scheme == LESB_TWINNED)
+    CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
+  ResidentBufs rb = h->rbufs();
+  CK(enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, halo_policy, h->partials, h->res_d,
+                 nullptr, h->st, nullptr, nullptr, &rb));
+  CK(cudaGetLastError());
+  if (residuals_out)
+    CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  rc = check_resident_err(h);
+  if (rc) return rc;
+  h->known_finite = false;
+  return LESB_OK;
+}
+
 // ---- the time step ----
 int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* in_w, int n_iter, int scheme,
               float omega, double* residuals_out, int* fail_stage) {

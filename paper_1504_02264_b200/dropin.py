@@ -1,0 +1,52 @@
+"""Install the CUDA path behind the reference's own operator API.
+
+The reference (gmcf_mini, pure Python) has no plugin registry: its callers
+resolve the hot-path functions through module globals at call time
+(``les_main`` calls ``step``, les.py:460; ``cli`` calls ``les.step``,
+cli.py:208, and ``sor.solve_pressure``, cli.py:234 and 253; ``press`` calls
+``sor.solve_pressure``, les.py:376).  ``install()`` rebinds those globals to
+this package's functions, which take the reference's own FlowState,
+WindProfile, Scheme and halo_fn objects; ``uninstall()``
+restores the originals.
+
+    import gmcf_mini
+    import paper_1504_02264_b200 as b200
+    b200.install()          # every les.step / solve_pressure now runs on the GPU
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import les as _les
+from . import sor as _sor
+
+LES_FUNCS = ("step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf", "les_viscosity",
+             "strain_magnitude", "adam", "divergence", "press")
+SOR_FUNCS = ("solve_pressure", "redblack_iteration", "twinned_sweep")
+
+_saved: dict = {}
+
+
+def install(les_module=None, sor_module=None) -> None:
+    """Rebind gmcf_mini.les / gmcf_mini.sor hot-path functions to the CUDA
+    implementations (idempotent)."""
+    lm = les_module or importlib.import_module("gmcf_mini.les")
+    sm = sor_module or importlib.import_module("gmcf_mini.sor")
+    for mod, names, impl in ((lm, LES_FUNCS, _les), (sm, SOR_FUNCS, _sor)):
+        for n in names:
+            key = (mod.__name__, n)
+            if key not in _saved:
+                _saved[key] = (mod, getattr(mod, n))
+            setattr(mod, n, getattr(impl, n))
+
+
+def uninstall() -> None:
+    """Restore the reference implementations."""
+    for (_modname, n), (mod, fn) in list(_saved.items()):
+        setattr(mod, n, fn)
+    _saved.clear()
+
+
+def installed() -> bool:
+    return bool(_saved)

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _native as N
 from . import runtime
-from .reftypes import Grid, NumericsError, Scheme, SorCoeffs
+from .reftypes import Grid, NumericsError, Scheme, SorCoeffs, is_redblack, is_twinned
 from .sor import PressureHalo, build_uniform_coeffs
 
 __all__ = [
@@ -315,9 +315,9 @@ def _pressure_halo(grid: Grid):
 
 
 def _scheme_code(scheme):
-    if scheme is Scheme.REDBLACK:
+    if is_redblack(scheme):
         return N.LESB_REDBLACK
-    if scheme is Scheme.TWINNED:
+    if is_twinned(scheme):
         return N.LESB_TWINNED
     raise ValueError(f"unknown scheme {scheme!r}")
 
@@ -328,7 +328,7 @@ def _check_solver_args(n_iter, scheme, workers):
         raise ValueError("n_iter must be >= 1")
     if workers < 1:
         raise ValueError("workers must be >= 1")
-    if scheme is Scheme.REDBLACK and workers > 1:
+    if is_redblack(scheme) and workers > 1:
         raise ValueError("REDBLACK supports workers=1 only; use TWINNED for parallel runs")
 
 
@@ -337,7 +337,7 @@ def press(state, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK, omega: floa
     """rhs = div(u)/dt; SOR with the press halo; p replaced in place.
     Returns the float64 residual history (les.py:358-381)."""
     if omega is None:
-        omega = 1.7 if scheme is Scheme.REDBLACK else 1.0
+        omega = 1.7 if is_redblack(scheme) else 1.0
     sch = _scheme_code(scheme)
     _check_solver_args(n_iter, scheme, workers)
     ds, target = _resolve(state)
@@ -386,14 +386,14 @@ def step(state, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK, work
     that leaves a non-finite value."""
     g = state.grid
     kp = inflow.kp if hasattr(inflow, "kp") else len(inflow.u)
-    bad_args = kp != g.km or n_iter < 1 or workers < 1 or (scheme is Scheme.REDBLACK and workers > 1)
-    if bad_args or scheme not in (Scheme.REDBLACK, Scheme.TWINNED):
+    bad_args = kp != g.km or n_iter < 1 or workers < 1 or (is_redblack(scheme) and workers > 1)
+    if bad_args or not (is_redblack(scheme) or is_twinned(scheme)):
         return _step_staged(state, inflow, n_iter, scheme, workers)
     arrs = _inflow_arrays(inflow, g.km)
     ds, target = _resolve(state)
     h = ds.handle()
     ds._ensure_coeffs(h)
-    omega = 1.7 if scheme is Scheme.REDBLACK else 1.0
+    omega = 1.7 if is_redblack(scheme) else 1.0
     stage = N.C.c_int(-1)
     rc = h.call("lesb_step", *[N.fptr(a) for a in arrs], int(n_iter), _scheme_code(scheme), float(omega), None,
                 N.C.byref(stage))
@@ -415,7 +415,7 @@ def run_steps(state, inflow, n_steps: int, n_iter: int = 50, scheme: Scheme = Sc
     ds, target = _resolve(state)
     h = ds.handle()
     ds._ensure_coeffs(h)
-    omega = 1.7 if scheme is Scheme.REDBLACK else 1.0
+    omega = 1.7 if is_redblack(scheme) else 1.0
     done = N.C.c_int(0)
     stage = N.C.c_int(-1)
     rc = h.call("lesb_run_steps", int(n_steps), N.fptr(np.ascontiguousarray(block)), len(profs), int(n_iter),

@@ -98,4 +98,24 @@ except Exception:  # noqa: BLE001
         def kp(self) -> int:
             return self.u.shape[0]
 
-__all__ = ["Scheme", "Grid", "SorCoeffs", "WindProfile", "NumericsError", "HAVE_REFERENCE"]
+def _scheme_member(scheme, name: str) -> bool:
+    """``scheme is Scheme.<name>`` for this module's Scheme and for the
+    reference's own (gmcf_mini.sor.Scheme), whichever the caller holds: the
+    reference compares by identity (sor.py:268, 273), and the drop-in must
+    accept the reference's members even when this package was imported before
+    gmcf_mini was importable."""
+    if scheme is getattr(Scheme, name):
+        return True
+    return type(scheme).__name__ == "Scheme" and getattr(scheme, "name", None) == name
+
+
+def is_redblack(scheme) -> bool:
+    return _scheme_member(scheme, "REDBLACK")
+
+
+def is_twinned(scheme) -> bool:
+    return _scheme_member(scheme, "TWINNED")
+
+
+__all__ = ["Scheme", "Grid", "SorCoeffs", "WindProfile", "NumericsError", "HAVE_REFERENCE", "is_redblack",
+           "is_twinned"]

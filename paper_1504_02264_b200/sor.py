@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as N
-from .reftypes import Grid, Scheme, SorCoeffs
+from .reftypes import Grid, Scheme, SorCoeffs, is_redblack
 
 __all__ = [
     "Grid", "Scheme", "SorCoeffs", "build_uniform_coeffs", "make_field", "make_twinned",
@@ -118,7 +118,7 @@ def solve_pressure(p0, rhs, c, omega, n_iter, scheme: Scheme, workers: int = 1, 
         raise ValueError("n_iter must be >= 1")
     if workers < 1:
         raise ValueError("workers must be >= 1")
-    if scheme is Scheme.REDBLACK and workers > 1:
+    if is_redblack(scheme) and workers > 1:
         raise ValueError("REDBLACK supports workers=1 only; use TWINNED for parallel runs")
     im, jm, km = _check_shapes(p0, rhs, c)
     policy = halo_policy(halo_fn, p0.shape)
@@ -128,7 +128,7 @@ def solve_pressure(p0, rhs, c, omega, n_iter, scheme: Scheme, workers: int = 1, 
     rhsc = N.f32c(rhs)
     p = np.empty_like(p0c)
     res = np.zeros(n_iter, dtype=np.float64)
-    sch = N.LESB_REDBLACK if scheme is Scheme.REDBLACK else N.LESB_TWINNED
+    sch = N.LESB_REDBLACK if is_redblack(scheme) else N.LESB_TWINNED
     N.check(N.load().lesb_solve_pressure(im, jm, km, N.fptr(p0c), N.fptr(rhsc), cf, float(omega), int(n_iter),
                                          sch, policy, N.fptr(p), N.dptr(res), _device()),
             "solve_pressure")

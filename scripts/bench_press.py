@@ -1,0 +1,78 @@
+"""Press-only SOR benchmark (BASELINE.json configs[2]).
+
+rhs[int] = default_rng(0).uniform(-1, 1) float32, p0 = 0, h = 1, red-black
+with omega = 1.7, n_iter iterations, halo_fn=None (sor-bench semantics,
+cli.py:222-283) or the press halo.  Inputs are device resident (uploaded once);
+each timed solve restores p0 with a device copy first (untimed) and is
+bracketed by CUDA events on the domain stream, with L2 flushed before it.
+
+  python scripts/bench_press.py [im jm km] [--path 0|1|2|3] [--n-iter 50] [--reps 5] [--halo stored|press]
+
+Prints one JSON line: M cell-iterations/s, us per iteration, and the HBM
+roofline fraction at 12 B per cell and iteration (p read + write, rhs read;
+cn1 is a scalar).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT]
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1504_02264_b200 as P  # noqa: E402
+from paper_1504_02264_b200 import _native as N  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("dims", nargs="*", type=int, default=[512, 512, 90])
+ap.add_argument("--path", type=int, default=0)
+ap.add_argument("--n-iter", type=int, default=50)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--halo", default="stored", choices=["stored", "press"])
+a = ap.parse_args()
+im, jm, km = a.dims
+P.runtime.set_sor_path(a.path)
+grid = P.Grid.uniform(im, jm, km, 1.0)
+fs = P.FlowState.create(grid, dt=1.0)
+h = fs.handle()
+fs._ensure_coeffs(h)
+lib = N.load()
+rng = np.random.default_rng(0)
+rhs = np.zeros((im + 2, jm + 2, km + 2), np.float32)
+rhs[1:-1, 1:-1, 1:-1] = rng.uniform(-1, 1, size=(im, jm, km)).astype(np.float32)
+N.check(lib.lesb_upload(h.h, N.LESB_RHS, N.fptr(rhs)), "upload rhs")
+p0 = np.zeros_like(rhs)
+policy = N.LESB_HALO_STORED if a.halo == "stored" else N.LESB_HALO_PRESS
+stream = torch.cuda.ExternalStream(lib.lesb_stream(h.h))
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+res = np.zeros(a.n_iter)
+times = []
+for r in range(a.reps + 1):
+    N.check(lib.lesb_upload(h.h, N.LESB_P, N.fptr(p0)), "upload p0")
+    with torch.cuda.stream(stream):
+        flush.fill_(float(r))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    N.check(lib.lesb_sor_solve(h.h, a.n_iter, N.LESB_REDBLACK, 1.7, policy, N.dptr(res)), "sor_solve")
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if r > 0:
+        times.append(e0.elapsed_time(e1))
+ms = min(times)
+n = im * jm * km
+peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+gbs = 12 * n * a.n_iter / (ms * 1e-3) / 1e9
+print(json.dumps({
+    "config": f"press-only {im}x{jm}x{km}, RB omega 1.7, {a.n_iter} iterations, halo {a.halo}",
+    "sor_kernel": {1: "k_sor_rb", 2: "k_sor_resident", 3: "k_sor_rbfused"}[lib.lesb_sor_path_in_use(h.h, 0)],
+    "ms_per_solve": ms, "us_per_iteration": 1000 * ms / a.n_iter,
+    "mcell_iter_per_s": n * a.n_iter / (ms * 1e-3) / 1e6,
+    "roofline": {"bytes_per_cell_iteration": 12, "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"],
+                 "frac": gbs / peaks["hbm_gbs"]},
+    "res_first_last": [float(res[0]), float(res[-1])],
+    "times_ms": times,
+}))

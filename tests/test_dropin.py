@@ -1,0 +1,71 @@
+"""The drop-in hook rebinds exactly the reference's hot-path functions and
+restores them (CPU only: no compute calls).  Needs the reference importable,
+which it is in the build container; skipped elsewhere (the GPU box)."""
+
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture()
+def ref():
+    if os.path.isdir(REF) and REF not in sys.path:
+        sys.path.append(REF)
+    les = pytest.importorskip("gmcf_mini.les")
+    sor = pytest.importorskip("gmcf_mini.sor")
+    return les, sor
+
+
+def test_install_rebinds_and_restores(ref):
+    les, sor = ref
+    import paper_1504_02264_b200 as P
+
+    orig = {n: getattr(les, n) for n in P.dropin.LES_FUNCS}
+    orig.update({n: getattr(sor, n) for n in P.dropin.SOR_FUNCS})
+    P.install()
+    try:
+        assert P.installed()
+        for n in P.dropin.LES_FUNCS:
+            assert getattr(les, n) is getattr(P.les, n), n
+        for n in P.dropin.SOR_FUNCS:
+            assert getattr(sor, n) is getattr(P.sor, n), n
+        P.install()  # idempotent: originals stay recorded
+    finally:
+        P.uninstall()
+    for n, fn in orig.items():
+        mod = les if n in P.dropin.LES_FUNCS else sor
+        assert getattr(mod, n) is fn, n
+    assert not P.installed()
+
+
+def test_reference_scheme_members_accepted(ref):
+    """Scheme is compared by identity in the reference (sor.py:268, 273); the
+    drop-in accepts the reference's own members as well as its own (the
+    package may have been imported before gmcf_mini was importable)."""
+    les, sor = ref
+    from paper_1504_02264_b200 import les as L
+    from paper_1504_02264_b200 import reftypes
+
+    assert reftypes.is_redblack(sor.Scheme.REDBLACK) and not reftypes.is_redblack(sor.Scheme.TWINNED)
+    assert reftypes.is_twinned(sor.Scheme.TWINNED)
+    assert reftypes.is_redblack(reftypes.Scheme.REDBLACK)
+    assert L._scheme_code(sor.Scheme.REDBLACK) == 0 and L._scheme_code(sor.Scheme.TWINNED) == 1
+    with pytest.raises(ValueError):
+        L._scheme_code("redblack")
+
+
+def test_reference_pressure_halo_maps_to_press_policy(ref):
+    les, sor = ref
+    from paper_1504_02264_b200 import _native as N
+    from paper_1504_02264_b200 import sor as S
+
+    grid = sor.Grid.uniform(4, 5, 3, 1.0)
+    assert S.halo_policy(les._pressure_halo(grid), (6, 7, 5)) == N.LESB_HALO_PRESS
+    assert S.halo_policy(None, (6, 7, 5)) == N.LESB_HALO_STORED
+    with pytest.raises(NotImplementedError):
+        S.halo_policy(lambda p: None, (6, 7, 5))
+    with pytest.raises(ValueError):
+        S.halo_policy(S.PressureHalo(grid), (6, 8, 5))
