@@ -36,3 +36,8 @@ per_pass = (t[:, 2:, 0].max(0)[1:] - t[:, 2:, 0].max(0)[:-1]) / 1e3
 print("pass period (max start over tiles) us: mean %.2f min %.2f max %.2f" % (per_pass.mean(), per_pass.min(), per_pass.max()))
 print("tile 0 passes 10-14 (recv, bnd, int):", [(round(a, 2), round(b, 2), round(c, 2)) for a, b, c in zip(d_recv[0, 10:15], d_bnd[0, 10:15], d_int[0, 10:15])])
 print("start skew across tiles at pass 50 (us): %.2f" % ((t[:, 50, 0].max() - t[:, 50, 0].min()) / 1e3))
+comp = (d_bnd + d_int)[:, 2:].mean(1)
+order = np.argsort(comp)
+print("per-tile compute (bnd+int) us: min %.2f median %.2f max %.2f" % (comp.min(), np.median(comp), comp.max()))
+print("slowest tiles:", [(int(t), round(float(comp[t]), 2)) for t in order[-6:]])
+print("fastest tiles:", [(int(t), round(float(comp[t]), 2)) for t in order[:4]])
