@@ -180,6 +180,21 @@ int lesb_redblack_iteration(int im, int jm, int km, float* p, const float* rhs,
 int lesb_twinned_sweep(int im, int jm, int km, const float* src, float* dst, const float* rhs,
                        const lesb_coeffs* c, float omega, double* residual, int device);
 
+/* ---- x-slab decomposition over several GPUs ----
+ * A slab is a domain created with i_offset / west_boundary / east_boundary
+ * describing its planes of the global grid.  After linking, lesb_step and
+ * lesb_press exchange the halo planes: velocities after velnw+bondv1 (depth 1
+ * low, 2 high), pressure after every colour pass / sweep and after the final
+ * halo.  Results equal the single-domain step bitwise. */
+/* ncclGetUniqueId into out (>= 128 bytes); returns the id size. */
+int lesb_nccl_unique_id(void* out, int nbytes);
+/* One process per GPU: rank r's neighbours are r-1 (west) and r+1 (east). */
+int lesb_link_nccl(lesb_handle h, const void* unique_id, int nranks, int rank);
+/* In-process slabs (west to east) on one device, stepped with lesb_group_step. */
+int lesb_link_local(lesb_handle* hs, int n);
+int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v, const float* in_w, int n_iter,
+                    int scheme, float omega, double* residuals_out, int* fail_stage);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nccl.h>
+
 #include "les_b200.h"
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
@@ -83,7 +85,17 @@ int first_stage(unsigned bits) {
 
 }  // namespace
 
+// Neighbours of an x-slab: in-process domains on the same
+// device (plane copies), or ranks rank-1 / rank+1 of an NCCL communicator.
+struct SlabLink {
+  lesb_domain* west = nullptr;
+  lesb_domain* east = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+};
+
 struct lesb_domain {
+  SlabLink link;
   int device = 0;
   cudaStream_t st = nullptr;
   Geo g{};
@@ -237,13 +249,53 @@ float* field_ptr(lesb_domain* h, int f) {
 
 long long field_count(lesb_domain* h, int f) { return (f == LESB_FGH || f == LESB_FGH_OLD) ? 3 * h->n_py : h->n_py; }
 
+// ---- x-slab halo exchange ----
+// Halo planes are contiguous (jm+2)(km+2) runs.  The low halo (plane 0) takes
+// the west neighbour's last interior plane; the high halo (planes im+1 ..
+// im+depth) takes the east neighbour's first `depth` planes.  Velocities use
+// depth 2 (velfg's shifted derivative at local i = im, les.py:100-110), the
+// pressure depth 1.
+ncclResult_t nccl_exchange(lesb_domain* h, float* f, int depth, cudaStream_t st) {
+  const size_t si = (size_t)h->g.si;
+  const int r = h->link.rank;
+  ncclResult_t e = ncclGroupStart();
+  if (e != ncclSuccess) return e;
+  if (!h->g.west_bc) {
+    ncclSend(f + si, depth * si, ncclFloat, r - 1, h->link.comm, st);
+    ncclRecv(f, si, ncclFloat, r - 1, h->link.comm, st);
+  }
+  if (!h->g.east_bc) {
+    ncclSend(f + (size_t)h->g.im * si, si, ncclFloat, r + 1, h->link.comm, st);
+    ncclRecv(f + (size_t)(h->g.im + 1) * si, depth * si, ncclFloat, r + 1, h->link.comm, st);
+  }
+  return ncclGroupEnd();
+}
+
+// in-process neighbours: copy the neighbours' planes of field `which` into h
+void local_exchange(lesb_domain* h, float* lesb_domain::*which, int depth, cudaStream_t st) {
+  const size_t si = (size_t)h->g.si, fb = si * sizeof(float);
+  float* f = h->*which;
+  if (h->link.west) {
+    const lesb_domain* w = h->link.west;
+    cudaMemcpyAsync(f, w->*which + (size_t)w->g.im * si, fb, cudaMemcpyDeviceToDevice, st);
+  }
+  if (h->link.east) cudaMemcpyAsync(f + (size_t)(h->g.im + 1) * si, h->link.east->*which + si, depth * fb,
+                                    cudaMemcpyDeviceToDevice, st);
+}
+
+void nccl_p_hook(void* ctx, float* p) {
+  lesb_domain* h = static_cast<lesb_domain*>(ctx);
+  nccl_exchange(h, p, 1, h->st);
+}
+
 // Enqueue the press stage on the stream: rhs = div(u)/dt, SOR, final halo.
 cudaError_t enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, bool rhs_from_state,
                           unsigned* flags) {
   if (rhs_from_state) launch_divergence(h->g, h->spac(), h->u, h->v, h->w, h->rhs, h->dt, 1, h->st);
   ResidentBufs rb = h->rbufs();
+  ExchangeHook hook{h->link.comm ? nccl_p_hook : nullptr, h};
   return enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d, flags, h->st,
-              nullptr, nullptr, &rb);
+                     &hook, nullptr, &rb);
 }
 
 // The full step: velnw+bondv1 (A -> B), velfg+feedbf+les+adam+rhs (B -> A), press.
@@ -257,11 +309,16 @@ cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omeg
   mark(0);
   launch_velnw_bondv1(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->inflow_d, h->ub, h->vb, h->wb,
                       flags, h->st);
+  if (h->link.comm) {  // x-slab: velocity halos after velnw + bondv1
+    nccl_exchange(h, h->ub, 2, h->st);
+    nccl_exchange(h, h->vb, 2, h->st);
+    nccl_exchange(h, h->wb, 2, h->st);
+  }
   mark(1);
   launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
                    h->vn, h->dt, h->cs != 0.0f, h->csd2, h->csd2s, flags, h->st);
   mark(2);
-  ExchangeHook hook{nullptr, nullptr};
+  ExchangeHook hook{h->link.comm ? nccl_p_hook : nullptr, h};
   SorMarks marks{h->timing ? h->ev[3] : nullptr};
   ResidentBufs rb = h->rbufs();
   cudaError_t e = enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials,
@@ -433,6 +490,9 @@ int lesb_destroy(lesb_handle h) {
   if (!h) return LESB_OK;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->link.comm) ncclCommDestroy(h->link.comm);
+  if (h->link.west) h->link.west->link.east = nullptr;
+  if (h->link.east) h->link.east->link.west = nullptr;
   clear_graphs(h);
   float* bufs[] = {h->u, h->v, h->w, h->ub, h->vb, h->wb, h->p, h->pb, h->rhs, h->mask, h->fgh, h->fgh_old,
                    h->dx1, h->dy1, h->dzn, h->inflow_d, h->scratch, h->csd2, h->cn1,
@@ -969,6 +1029,142 @@ int lesb_twinned_sweep(int im, int jm, int km, const float* src, float* dst, con
   if (residual) CK(cudaMemcpyAsync(residual, h->res_d, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return LESB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// x-slab decomposition
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int lesb_nccl_unique_id(void* out, int nbytes) {
+  if (!out || nbytes < (int)sizeof(ncclUniqueId)) return fail(LESB_E_ARG, "unique-id buffer too small");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(LESB_E_CUDA, "ncclGetUniqueId failed");
+  std::memcpy(out, &id, sizeof(id));
+  return (int)sizeof(ncclUniqueId);
+}
+
+int lesb_link_nccl(lesb_handle h, const void* id, int nranks, int rank) {
+  if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(LESB_E_ARG, "bad argument");
+  if ((rank > 0) == (bool)h->g.west_bc || (rank < nranks - 1) == (bool)h->g.east_bc)
+    return fail(LESB_E_ARG, "slab boundaries do not match the rank's position");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  const ncclResult_t e = ncclCommInitRank(&comm, nranks, uid, rank);
+  if (e != ncclSuccess) return fail(LESB_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(e));
+  h->link.comm = comm;
+  h->link.rank = rank;
+  h->link.nranks = nranks;
+  clear_graphs(h);
+  return LESB_OK;
+}
+
+int lesb_link_local(lesb_handle* hs, int n) {
+  if (!hs || n < 1) return fail(LESB_E_ARG, "bad argument");
+  for (int s = 0; s < n; ++s) {
+    if (!hs[s]) return fail(LESB_E_ARG, "null handle");
+    if (hs[s]->device != hs[0]->device) return fail(LESB_E_ARG, "in-process slabs must share a device");
+    if ((s > 0) == (bool)hs[s]->g.west_bc || (s < n - 1) == (bool)hs[s]->g.east_bc)
+      return fail(LESB_E_ARG, "slab boundaries do not match the slab's position");
+    if (s > 0 && (hs[s]->g.jm != hs[0]->g.jm || hs[s]->g.km != hs[0]->g.km ||
+                  hs[s]->g.ioff != hs[s - 1]->g.ioff + hs[s - 1]->g.im))
+      return fail(LESB_E_ARG, "slabs must tile the x axis in order");
+    hs[s]->link.west = s > 0 ? hs[s - 1] : nullptr;
+    hs[s]->link.east = s < n - 1 ? hs[s + 1] : nullptr;
+  }
+  return LESB_OK;
+}
+
+// One step of n in-process slabs, all enqueued on the first slab's stream:
+// each phase runs on every slab before the halo planes move.  Red-black and
+// twinned use the streaming kernels (the resident / fused solvers need the
+// whole grid).  Results equal one domain's step bitwise; residuals (summed
+// over slabs in order) agree to summation-order tolerance.
+int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v, const float* in_w, int n_iter,
+                    int scheme, float omega, double* residuals_out, int* fail_stage) {
+  if (!hs || n < 1 || !in_u || !in_v || !in_w) return fail(LESB_E_ARG, "bad argument");
+  for (int s = 0; s < n; ++s) {
+    int rc = check_args_step(hs[s], n_iter, scheme);
+    if (rc) return rc;
+  }
+  lesb_domain* h0 = hs[0];
+  CK(cudaSetDevice(h0->device));
+  cudaStream_t st = h0->st;
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    CK(cudaStreamSynchronize(h->st));
+    int rc = ensure_partials(h, n_iter);
+    if (rc) return rc;
+    const int km = h->g.km;
+    std::memcpy(h->inflow_h, in_u, km * sizeof(float));
+    std::memcpy(h->inflow_h + km, in_v, km * sizeof(float));
+    std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
+    CK(cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * km * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), st));
+  }
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    launch_velnw_bondv1(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->inflow_d, h->ub, h->vb, h->wb,
+                        &h->book_d->flags, st);
+  }
+  for (int s = 0; s < n; ++s) {
+    local_exchange(hs[s], &lesb_domain::ub, 2, st);
+    local_exchange(hs[s], &lesb_domain::vb, 2, st);
+    local_exchange(hs[s], &lesb_domain::wb, 2, st);
+  }
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
+                     h->vn, h->dt, h->cs != 0.0f, h->csd2, h->csd2s, &h->book_d->flags, st);
+    if (scheme == LESB_TWINNED)
+      CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  for (int it = 0; it < n_iter; ++it) {
+    for (int nrd = 0; nrd < 2; ++nrd) {
+      for (int s = 0; s < n; ++s) {
+        lesb_domain* h = hs[s];
+        const int nblk = scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g);
+        double* part = h->partials + ((long long)it * 2 + nrd) * nblk;
+        if (scheme == LESB_REDBLACK) {
+          launch_rb_pass(h->g, h->p, h->rhs, h->sorc(), omega, nrd, 1, part, st);
+        } else {
+          launch_tw_sweep(h->g, nrd == 0 ? h->p : h->pb, nrd == 0 ? h->pb : h->p, h->rhs, h->sorc(), omega, 1,
+                          part, st);
+        }
+      }
+      for (int s = 0; s < n; ++s)
+        local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
+    }
+  }
+  for (int s = 0; s < n; ++s) launch_press_halo(hs[s]->g, hs[s]->p, &hs[s]->book_d->flags, st);
+  for (int s = 0; s < n; ++s) local_exchange(hs[s], &lesb_domain::p, 1, st);
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    launch_reduce_res(h->partials, scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g), n_iter,
+                      h->res_d, st);
+    CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  unsigned bits = 0;
+  for (int s = 0; s < n; ++s) {
+    bits |= hs[s]->book_h->flags;
+    hs[s]->known_finite = false;
+  }
+  if (residuals_out)
+    for (int it = 0; it < n_iter; ++it) {
+      double t = 0.0;
+      for (int s = 0; s < n; ++s) t += hs[s]->res_h[it];
+      residuals_out[it] = t;
+    }
+  if (fail_stage) *fail_stage = bits ? first_stage(bits) : -1;
+  return bits ? LESB_NONFINITE : LESB_OK;
 }
 
 }  // extern "C"

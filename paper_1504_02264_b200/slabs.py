@@ -1,0 +1,208 @@
+"""x-slab decomposition of the LES step over several GPUs.
+
+The grid is cut along x (the slowest axis) into slabs of whole (j, k) planes,
+so every halo exchange moves contiguous (jm+2)(km+2) planes; y stays local,
+so the periodic wrap stays a local remap.  The kernels see a slab through its
+geometry (``i_offset`` for the global red-black colour, ``west/east_boundary``
+for which x faces are physical) and keep a depth-2 high-x velocity halo for
+velfg's shifted derivative (les.py:100-110).  The exchange schedule is the
+one SURVEY 8(e) verified by CPU emulation: velocities after velnw + bondv1
+(depth 1 low, 2 high), pressure after every colour pass / sweep and after the
+final halo, residuals summed once per press, stage flags OR-ed once per step.
+
+Two drivers over the same C ABI:
+  * ``SlabGroup``: n slabs in one process on one device, stepped together
+    with plane copies (lesb_group_step) -- the single-GPU bitwise check of
+    the decomposition;
+  * ``SlabDomain``: one slab per process / GPU, NCCL send/recv of the halo
+    planes inside the step's CUDA graph (lesb_link_nccl); the unique id and
+    the stage-flag / residual reductions go through torch.distributed.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .les import _FIELD_ID, _csd2, _inflow_arrays, _scheme_code
+from .reftypes import Grid, NumericsError, Scheme, is_redblack
+from .sor import build_uniform_coeffs
+
+FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p", "mask")
+STATE = ("u", "v", "w", "fgh", "fgh_old", "p")
+
+
+def slab_bounds(im: int, nslabs: int, s: int) -> tuple[int, int]:
+    """Global interior planes [i0, i1] (1-based, inclusive) of slab s: the
+    first im % nslabs slabs get one plane more."""
+    if not 1 <= nslabs <= im:
+        raise ValueError(f"cannot cut {im} planes into {nslabs} slabs")
+    base, extra = divmod(im, nslabs)
+    i0 = 1 + s * base + min(s, extra)
+    return i0, i0 + base + (1 if s < extra else 0) - 1
+
+
+def halo_plan(im_local: int, west: bool, east: bool, depth: int):
+    """The plane exchange one slab performs (mirrors capi.cu nccl_exchange):
+    a list of (op, peer, first local plane, number of planes) with peer -1 =
+    west, +1 = east.  Used by the CPU tests to check the schedule."""
+    plan = []
+    if west:
+        plan += [("send", -1, 1, depth), ("recv", -1, 0, 1)]
+    if east:
+        plan += [("send", +1, im_local, 1), ("recv", +1, im_local + 1, depth)]
+    return plan
+
+
+def slice_global(arr: np.ndarray, i0: int, i1: int) -> np.ndarray:
+    """The slab's Python-visible array: global planes i0-1 .. i1+1."""
+    return np.ascontiguousarray(arr[i0 - 1:i1 + 2])
+
+
+def gather(parts: list[np.ndarray], bounds: list[tuple[int, int]]) -> np.ndarray:
+    """Global array from slab arrays: interior planes from their owners, the
+    west halo plane from the first slab, the east one from the last."""
+    first = parts[0]
+    im = bounds[-1][1]
+    out = np.empty((im + 2,) + first.shape[1:], first.dtype)
+    out[0] = parts[0][0]
+    for part, (i0, i1) in zip(parts, bounds):
+        out[i0:i1 + 1] = part[1:i1 - i0 + 2]
+    out[im + 1] = parts[-1][-1]
+    return out
+
+
+class _Slab:
+    """One slab domain (lesb_handle) with its geometry."""
+
+    def __init__(self, grid: Grid, dt, vn, cs, i0: int, i1: int, device: int):
+        lib = N.load()
+        self.lib = lib
+        self.i0, self.i1 = i0, i1
+        im = i1 - i0 + 1
+        self.im = im
+        g = grid
+        # spacings: global dx1[i0-1 .. i1+2] (im+3 entries)
+        dx = np.asarray(g.dx1, np.float32)
+        self._keep = [np.ascontiguousarray(dx[i0 - 1:i1 + 3]), N.f32c(g.dy1), N.f32c(g.dzn)]
+        csd2, csd2s = _csd2(g, cs)
+        if csd2 is not None:
+            csd2 = np.ascontiguousarray(csd2[i0 - 1:i1])
+            self._keep.append(csd2)
+        desc = N.lesb_desc(im, g.jm, g.km, i0 - 1, int(i0 == 1), int(i1 == g.im),
+                           *[N.fptr(a) for a in self._keep[:3]], float(dt), float(vn), float(cs),
+                           N.fptr(csd2), csd2s, int(device))
+        h = N.C.c_void_p()
+        N.check(lib.lesb_create(N.C.byref(desc), N.C.byref(h)), "lesb_create")
+        self.h = h
+        c = build_uniform_coeffs(g)
+        keep: list = []
+        cf = N.make_coeffs(c, keep)
+        # coefficient vectors restricted to the slab (cn2l/cn2s are per x plane)
+        if cf.cn1:
+            raise NotImplementedError("slabs need a scalar cn1 (uniform grids)")
+        ax = [np.ascontiguousarray(np.asarray(getattr(c, n), np.float32)[i0 - 1:i1]) for n in ("cn2l", "cn2s")]
+        keep.extend(ax)
+        cf.cn2l, cf.cn2s = N.fptr(ax[0]), N.fptr(ax[1])
+        N.check(lib.lesb_set_coeffs(h, N.C.byref(cf)), "lesb_set_coeffs")
+
+    def upload(self, name, global_arr):
+        part = slice_global(np.asarray(global_arr, np.float32), self.i0, self.i1)
+        N.check(self.lib.lesb_upload(self.h, _FIELD_ID[name], N.fptr(part)), "lesb_upload")
+
+    def download(self, name, jm, km):
+        shape = (self.im + 2, jm + 2, km + 2) + ((3,) if name in ("fgh", "fgh_old") else ())
+        out = np.empty(shape, np.float32)
+        N.check(self.lib.lesb_download(self.h, _FIELD_ID[name], N.fptr(out)), "lesb_download")
+        return out
+
+    def close(self):
+        if self.h is not None:
+            self.lib.lesb_destroy(self.h)
+            self.h = None
+
+
+class SlabGroup:
+    """``nslabs`` x-slabs of one grid in this process, on one device."""
+
+    def __init__(self, grid: Grid, nslabs: int, dt: float, vn: float = 1e-5, cs: float = 0.14, device: int = 0):
+        self.grid = grid
+        self.bounds = [slab_bounds(grid.im, nslabs, s) for s in range(nslabs)]
+        self.slabs = [_Slab(grid, dt, vn, cs, i0, i1, device) for i0, i1 in self.bounds]
+        arr = (N.C.c_void_p * nslabs)(*[s.h for s in self.slabs])
+        self._arr = arr
+        N.check(N.load().lesb_link_local(arr, nslabs), "lesb_link_local")
+
+    def upload(self, state: dict):
+        for name in FIELDS:
+            for s in self.slabs:
+                s.upload(name, state[name])
+
+    def step(self, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK):
+        g = self.grid
+        arrs = _inflow_arrays(inflow, g.km)
+        res = np.zeros(n_iter, np.float64)
+        stage = N.C.c_int(-1)
+        omega = 1.7 if is_redblack(scheme) else 1.0
+        rc = N.check(N.load().lesb_group_step(self._arr, len(self.slabs), *[N.fptr(a) for a in arrs], int(n_iter),
+                                              _scheme_code(scheme), float(omega), N.dptr(res), N.C.byref(stage)),
+                     "lesb_group_step")
+        if rc == N.LESB_NONFINITE:
+            raise NumericsError(N.STAGE_NAMES[stage.value], "device stage check (slabs)")
+        return res
+
+    def gather(self, name: str) -> np.ndarray:
+        g = self.grid
+        return gather([s.download(name, g.jm, g.km) for s in self.slabs], self.bounds)
+
+    def close(self):
+        for s in self.slabs:
+            s.close()
+
+
+class SlabDomain:
+    """This rank's x-slab in a one-process-per-GPU run (torch.distributed
+    initialised; NCCL for the device exchanges)."""
+
+    def __init__(self, grid: Grid, dt: float, vn: float = 1e-5, cs: float = 0.14, device: int = 0):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
+        self.grid = grid
+        self.bounds = [slab_bounds(grid.im, self.nranks, s) for s in range(self.nranks)]
+        i0, i1 = self.bounds[self.rank]
+        self.slab = _Slab(grid, dt, vn, cs, i0, i1, device)
+        uid = N.C.create_string_buffer(128)
+        if self.rank == 0:
+            N.check(N.load().lesb_nccl_unique_id(uid, 128), "lesb_nccl_unique_id")
+        box = [uid.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = N.C.create_string_buffer(box[0], 128)
+        N.check(N.load().lesb_link_nccl(self.slab.h, uid, self.nranks, self.rank), "lesb_link_nccl")
+
+    def upload(self, state: dict):
+        for name in FIELDS:
+            self.slab.upload(name, state[name])
+
+    def step(self, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK) -> None:
+        """One step; every rank raises the same NumericsError (stage bits are
+        OR-reduced over ranks)."""
+        import torch
+
+        g = self.grid
+        arrs = _inflow_arrays(inflow, g.km)
+        stage = N.C.c_int(-1)
+        omega = 1.7 if is_redblack(scheme) else 1.0
+        rc = N.check(self.slab.lib.lesb_step(self.slab.h, *[N.fptr(a) for a in arrs], int(n_iter),
+                                             _scheme_code(scheme), float(omega), None, N.C.byref(stage)),
+                     "lesb_step")
+        # the reference raises after the first stage (in step order) that left a
+        # non-finite value anywhere in the grid: the minimum over ranks
+        first = torch.tensor([stage.value if rc == N.LESB_NONFINITE else 99], dtype=torch.int64)
+        self.dist.all_reduce(first, op=self.dist.ReduceOp.MIN)
+        if int(first.item()) < 99:
+            raise NumericsError(N.STAGE_NAMES[int(first.item())], "device stage check (slabs)")
+
+    def close(self):
+        self.slab.close()

@@ -1,0 +1,82 @@
+"""x-slab decomposition on one B200: n slabs stepped in one process with
+halo-plane copies (lesb_group_step) must reproduce the single-domain step
+bitwise for every field (halos included), report the same blow-up step and
+stage, and give the same residuals to summation-order tolerance."""
+
+import numpy as np
+import pytest
+
+import golden_inputs as gi
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p")
+
+
+def bits_equal(a, b):
+    return a.shape == b.shape and np.array_equal(np.ascontiguousarray(a).view(np.uint32),
+                                                 np.ascontiguousarray(b).view(np.uint32))
+
+
+def single(P, st, inflow, n_steps, n_iter, scheme):
+    g = P.Grid(st["im"], st["jm"], st["km"], st["dx1"], st["dy1"], st["dzn"])
+    fs = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    for n in FIELDS + ("mask",):
+        getattr(fs, n)[...] = st[n]
+    out = []
+    for _ in range(n_steps):
+        P.les.step(fs, P.WindProfile(*inflow), n_iter=n_iter, scheme=scheme)
+        out.append({n: getattr(fs, n).copy() for n in FIELDS})
+    return out
+
+
+@pytest.mark.parametrize("dims,nslabs,scheme", [
+    ((24, 10, 8), 2, "redblack"),
+    ((24, 10, 8), 3, "redblack"),
+    ((9, 7, 5), 3, "redblack"),      # odd jm, uneven slabs
+    ((16, 12, 10), 4, "twinned"),
+    ((32, 32, 16), 4, "redblack"),
+])
+def test_slabs_equal_single_domain(dims, nslabs, scheme):
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200.slabs import SlabGroup
+
+    P.runtime.set_sor_path(0)
+    st = gi.random_state(*dims, seed=sum(dims) * 7 + nslabs, vel_scale=0.3)
+    inflow = gi.random_inflow(dims[2], seed=5)
+    sch = P.Scheme(scheme)
+    ref = single(P, st, inflow, 3, 12, sch)
+    g = P.Grid(*dims, st["dx1"], st["dy1"], st["dzn"])
+    grp = SlabGroup(g, nslabs, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    try:
+        grp.upload(st)
+        for s in range(3):
+            grp.step(P.WindProfile(*inflow), n_iter=12, scheme=sch)
+            for n in FIELDS:
+                got = grp.gather(n)
+                assert bits_equal(got, ref[s][n]), (dims, nslabs, s, n)
+    finally:
+        grp.close()
+
+
+def test_slabs_config1_blowup():
+    """Config 1 (32x32x16, one building straddling slabs): same hashes at
+    step 10 and the same blow-up step and stage (17, velfg) as one domain."""
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200.slabs import SlabGroup
+
+    st = gi.config1_state()
+    g = P.Grid(32, 32, 16, st["dx1"], st["dy1"], st["dzn"])
+    grp = SlabGroup(g, 3, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    try:
+        grp.upload(st)
+        inflow = P.WindProfile(*gi.default_inflow(16))
+        step = 0
+        with pytest.raises(P.NumericsError) as err:
+            while step < 40:
+                grp.step(inflow)
+                step += 1
+        assert step + 1 == 17
+        assert err.value.stage == "velfg"
+    finally:
+        grp.close()
