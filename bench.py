@@ -24,9 +24,10 @@ Arms
                oracle/ (the reference is pure Python/numpy; single-threaded
                RB path, 1 core), a bounded sample of full-size steps.
 
-Multi-GPU (torchrun, N > 1): replicas -- each rank runs the 150x150x90
-workload on its own GPU ("scaling": "weak"); value sums steps over ranks
-divided by the max-over-ranks time.
+Multi-GPU (torchrun, N > 1): x-slab decomposition -- each
+rank owns a 150x150x90 slab of a (150 N)x150x90 grid ("scaling": "weak"),
+halo planes move by NCCL send/recv inside the step's CUDA graph; value
+counts slab-steps over all ranks divided by the max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -188,20 +189,44 @@ def run_gpu(args):
     P.runtime.set_device(local)
     lib = N.load()
     st0 = gi.config2_state()
-    grid = P.Grid(IM, JM, KM, st0["dx1"], st0["dy1"], st0["dzn"])
     inflow = P.WindProfile(*gi.default_inflow(KM))
+    slab_dom = None
+    if world == 1:
+        grid = P.Grid(IM, JM, KM, st0["dx1"], st0["dy1"], st0["dzn"])
 
-    def make_state():
-        fs = P.FlowState.create(grid, dt=0.5, vn=0.8, cs=0.14)
-        fs.mask[...] = st0["mask"]
-        return fs
+        def make_state():
+            fs = P.FlowState.create(grid, dt=0.5, vn=0.8, cs=0.14)
+            fs.mask[...] = st0["mask"]
+            return fs
 
-    pristine = make_state()
-    hp = pristine.handle()
-    pristine._ensure_coeffs(hp)
-    work = make_state()
-    hw = work.handle()
-    work._ensure_coeffs(hw)
+        pristine = make_state()
+        hp = pristine.handle()
+        pristine._ensure_coeffs(hp)
+        work = make_state()
+        hw = work.handle()
+        work._ensure_coeffs(hw)
+    else:
+        # x-slabs: every rank owns a 150x150x90 slab of a (150 N)x150x90 grid
+        # with the 3x3 building array repeated per slab; halo planes move by
+        # NCCL send/recv inside the step graph
+        from paper_1504_02264_b200.slabs import SlabDomain, _Slab
+
+        grid = P.Grid.uniform(IM * world, JM, KM, 2.0)
+        gstate = gi.zero_state(IM * world, JM, KM)
+        for r in range(world):
+            gstate["mask"][1 + r * IM:1 + (r + 1) * IM] = st0["mask"][1:IM + 1]
+        slab_dom = SlabDomain(grid, dt=0.5, vn=0.8, cs=0.14, device=local)
+        slab_dom.upload(gstate)
+        i0, i1 = slab_dom.bounds[rank]
+        pristine = _Slab(grid, 0.5, 0.8, 0.14, i0, i1, local)
+        for name in ("u", "v", "w", "fgh", "fgh_old", "p", "mask"):
+            pristine.upload(name, gstate[name])
+
+        class _H:
+            def __init__(self, h):
+                self.h = h
+
+        hw, hp = _H(slab_dom.slab.h), _H(pristine.h)
     arrs = [N.f32c(getattr(inflow, c)) for c in ("u", "v", "w")]
     N.check(lib.lesb_set_inflow(hw.h, *[N.fptr(a) for a in arrs]), "set_inflow")
     N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
@@ -265,7 +290,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
     ms_per_step = dev_ms / args.steps
-    value = world * args.steps / (dev_ms / 1000.0)  # replicas: steps over all ranks / max time
+    value = world * args.steps / (dev_ms / 1000.0)  # slab-steps over all ranks / max time
     n_int = IM * JM * KM
     hbm, peak_kind = peaks()
     phase_ms /= args.steps
@@ -285,11 +310,16 @@ def run_gpu(args):
         traffic = None
 
     # ---- e2e through the public API ----
-    e2e = (e2e_run(P, N, gi, torch, grid, st0, inflow, args) if not args.no_e2e
-           else {"value": None, "seconds": 0.0, "h2d": 0, "d2h": 0})
-    if world > 1:
+    if args.no_e2e:
+        e2e = {"value": None, "seconds": 0.0, "h2d": 0, "d2h": 0}
+    elif slab_dom is None:
+        e2e = e2e_run(P, N, gi, torch, grid, st0, inflow, args)
+    else:
+        e2e = e2e_slabs(slab_dom, gstate, inflow, torch, args, world)
+    if world > 1 and e2e["value"] is not None:
         t = torch.tensor([e2e["seconds"]], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["value"] *= e2e["seconds"] / float(t.item())
         e2e["seconds"] = float(t.item())
 
     cpu = None
@@ -305,7 +335,9 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack",
                        "l2": "flushed before every timed step (256 MB device write, untimed)",
-                       "reinit_every_steps": REINIT, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "reinit_every_steps": REINIT,
+                       "parallelism": (f"x-slabs over {world} GPUs, {IM}x{JM}x{KM} per GPU, NCCL halo planes"
+                                       if world > 1 else "1 GPU"),
                        "timing": "CUDA events on the domain stream around each CUDA-graph step replay",
                        "sor_kernel": sor_path},
             "mlups": value * n_int / 1e6,
@@ -363,6 +395,32 @@ def e2e_run(P, N, gi, torch, grid, st0, inflow, args):
     h2d = sum(work[n].nbytes for n in names) / REINIT + 3 * KM * 4
     d2h = sum(work[n].nbytes for n in names[:6]) / REINIT + 4 + 8 * N_ITER
     return {"value": n_windows * REINIT / secs, "seconds": secs, "h2d": int(h2d), "d2h": int(d2h)}
+
+
+def e2e_slabs(dom, gstate, inflow, torch, args, world):
+    """Public slab API with host buffers (upload, steps, download) per window."""
+    names = ("u", "v", "w", "fgh", "fgh_old", "p", "mask")
+
+    def window():
+        dom.upload(gstate)
+        for _s in range(REINIT):
+            dom.step(inflow)
+        for n in names[:6]:
+            dom.slab.download(n, JM, KM)
+
+    window()
+    n_windows = max(1, args.steps // REINIT)
+    secs = 0.0
+    for _ in range(n_windows):
+        torch.cuda.synchronize()
+        dom.dist.barrier()
+        t0 = time.perf_counter()
+        window()
+        secs += time.perf_counter() - t0
+    per_slab = sum(gstate[n].nbytes for n in names) / world
+    h2d = per_slab / REINIT + 3 * KM * 4
+    d2h = per_slab * 6 / 7 / REINIT + 4
+    return {"value": world * n_windows * REINIT / secs, "seconds": secs, "h2d": int(h2d), "d2h": int(d2h)}
 
 
 def main():
