@@ -155,9 +155,9 @@ int lesb_copy_state(lesb_handle dst, lesb_handle src);
 int lesb_set_timing(lesb_handle h, int on);
 /* Red-black solver implementation: 0 auto (shared-memory-resident persistent
  * kernel when the grid fits the SMs' shared memory and the coefficients are
- * uniform, else the colour-fused streaming kernel, else colour passes),
- * 1 colour passes only, 2 resident when possible, 3 colour-fused when
- * possible.  Results are bitwise identical whichever runs. */
+ * uniform, else colour passes), 1 colour passes only, 2 resident when
+ * possible, 3 colour-fused streaming iterations when possible.  Results are
+ * bitwise identical whichever runs. */
 int lesb_set_sor_path(lesb_handle h, int path);
 int lesb_sor_path_in_use(lesb_handle h, int scheme);  /* 1 passes, 2 resident, 3 fused */
 /* Default for domains created afterwards and for the host-buffer solver

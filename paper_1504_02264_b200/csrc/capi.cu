@@ -137,8 +137,11 @@ struct lesb_domain {
     return SorC{cn1, cn1s, cn[0], cn[1], cn[2], cn[3], cn[4], cn[5], cuni, cw[0], cw[1], cw[2], cw[3], cw[4], cw[5]};
   }
   ResidentBufs rbufs() const {
+    // auto: the resident solver where the grid fits the SMs' shared memory,
+    // else the unfused colour passes (fastest streaming option measured so
+    // far, profiles/r1_v3_summary.md); the colour-fused kernel on request
     const bool res = (sor_path == 0 || sor_path == 2) && xbuf != nullptr;
-    const bool fz = sor_path == 3 || (sor_path == 0 && !res);
+    const bool fz = sor_path == 3;
     return ResidentBufs{res, device, fz ? 1 : 0, xbuf, repoch, &book_d->err};
   }
   long long n_int() const { return (long long)g.im * g.jm * g.km; }
@@ -184,7 +187,7 @@ void set_spacing_info(lesb_domain* h, const float* dx, const float* dy, const fl
 int ensure_partials(lesb_domain* h, int n_iter) {
   long long need = (long long)n_iter * 2 *
                    std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_partials(h->g, h->device)),
-                            sor_blocks_fused(h->g, h->device));
+                            std::max(sor_blocks_fused(h->g, h->device), sor_blocks_march(h->g, h->device)));
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
     h->partials = nullptr;
@@ -893,7 +896,7 @@ int lesb_sor_path_in_use(lesb_handle h, int scheme) {
   if (scheme != LESB_REDBLACK || h->sor_path == 1 || !h->coeffs_set) return 1;
   const bool res = (h->sor_path == 0 || h->sor_path == 2) && resident_supported(h->g, h->sorc(), h->device);
   if (res) return 2;
-  if ((h->sor_path == 0 || h->sor_path == 3) && fused_supported(h->g, h->sorc(), h->device)) return 3;
+  if (h->sor_path == 3 && fused_supported(h->g, h->sorc(), h->device)) return 3;
   return 1;
 }
 

@@ -76,6 +76,12 @@ int sor_blocks_fused(const Geo& g, int device);
 cudaError_t launch_rb_fused(const Geo& g, int device, const float* pa, float* pb, const float* rhs, const SorC& cf,
                             float om, int policy, double* partials, cudaStream_t st);
 
+// sor_march.cu
+bool march_supported(const Geo& g, const SorC& cf, int device);
+int sor_blocks_march(const Geo& g, int device);
+cudaError_t launch_rb_march(const Geo& g, int device, const float* pa, float* pb, const float* rhs, const SorC& cf,
+                            float om, int policy, double* partials, cudaStream_t st);
+
 // sor_resident.cu
 bool resident_supported(const Geo& g, const SorC& cf, int device);
 int resident_ntiles(const Geo& g, int device);

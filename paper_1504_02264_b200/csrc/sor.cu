@@ -19,6 +19,8 @@
 //          snapshotted before each pass instead (k_refresh_y) and read stored.
 //          One materialisation (k_press_halo) after the last pass reproduces
 //          the reference's final halo_fn call, including edges and corners.
+#include <cstdlib>
+
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
 
@@ -246,15 +248,21 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
     return cudaGetLastError();
   }
   if (scheme == 0 && res && res->fused && !(hook && hook->fn) && fused_supported(g, cf, res->device)) {
-    // colour-fused out-of-place iterations, ping-pong p <-> pb
-    const int nb = sor_blocks_fused(g, res->device);
+    // colour-fused out-of-place iterations, ping-pong p <-> pb: the i-marching
+    // kernel, or the tile kernel where the marching one does not fit
+    // the marching kernel is experimental (slower than the tile kernel on
+    // B200 so far, profiles/r1_v3_summary.md): opt in with LESB_SOR_MARCH=1
+    const bool march = march_supported(g, cf, res->device) && getenv("LESB_SOR_MARCH") &&
+                       std::atoi(getenv("LESB_SOR_MARCH")) != 0;
+    const int nb = march ? sor_blocks_march(g, res->device) : sor_blocks_fused(g, res->device);
     const size_t bytes = (size_t)(g.im + 2) * g.si * sizeof(float);
     cudaError_t e = cudaMemcpyAsync(pb, p, bytes, cudaMemcpyDeviceToDevice, st);  // pb's halo = stored halo
     if (e != cudaSuccess) return e;
     for (int it = 0; it < n_iter; ++it) {
       const float* src = (it & 1) ? pb : p;
       float* dst = (it & 1) ? p : pb;
-      e = launch_rb_fused(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st);
+      e = march ? launch_rb_march(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st)
+                : launch_rb_fused(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st);
       if (e != cudaSuccess) return e;
     }
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
