@@ -29,43 +29,56 @@ namespace lesb {
 constexpr int RB_BX = 32, RB_BY = 8;       // x: colour index along k, y: j
 constexpr int RB_NW = RB_BX * RB_BY / 32;
 
-template <int POL>
+template <int POL, bool UNI = false, typename IDX = long long>
 __device__ __forceinline__ float sor_point(const Geo& g, const float* __restrict__ p, const float* __restrict__ rhs,
-                                           const SorC& cf, float om, long long c, int i, int j, int k, int y_stored,
+                                           const SorC& cf, float om, IDX c, int i, int j, int k, int y_stored,
                                            float& pc_out) {
+  const IDX si = (IDX)g.si, sj = (IDX)g.sj;
   const float pc = p[c];
   float pE, pW, pN, pS, pT, pB;
   if (POL == 1) {
-    pE = (i == g.im && g.east_bc) ? 0.0f : p[c + g.si];
-    pW = (i == 1 && g.west_bc) ? pc : p[c - g.si];
-    pN = (j == g.jm && !y_stored) ? p[c - (long long)(g.jm - 1) * g.sj] : p[c + g.sj];
-    pS = (j == 1 && !y_stored) ? p[c + (long long)(g.jm - 1) * g.sj] : p[c - g.sj];
+    pE = (i == g.im && g.east_bc) ? 0.0f : p[c + si];
+    pW = (i == 1 && g.west_bc) ? pc : p[c - si];
+    pN = (j == g.jm && !y_stored) ? p[c - (IDX)(g.jm - 1) * sj] : p[c + sj];
+    pS = (j == 1 && !y_stored) ? p[c + (IDX)(g.jm - 1) * sj] : p[c - sj];
     pT = (k == g.km) ? 0.0f : p[c + 1];
     pB = (k == 1) ? pc : p[c - 1];
   } else {
-    pE = p[c + g.si];
-    pW = p[c - g.si];
-    pN = p[c + g.sj];
-    pS = p[c - g.sj];
+    pE = p[c + si];
+    pW = p[c - si];
+    pN = p[c + sj];
+    pS = p[c - sj];
     pT = p[c + 1];
     pB = p[c - 1];
   }
   // sor.py:164-171: E, W, N, S, T, B summed left to right
-  float nb = cf.cn2l[i - 1] * pE;
-  nb = nb + cf.cn2s[i - 1] * pW;
-  nb = nb + cf.cn3l[j - 1] * pN;
-  nb = nb + cf.cn3s[j - 1] * pS;
-  nb = nb + cf.cn4l[k - 1] * pT;
-  nb = nb + cf.cn4s[k - 1] * pB;
-  const float cn1 = cf.cn1 ? cf.cn1[((long long)(i - 1) * g.jm + (j - 1)) * g.km + (k - 1)] : cf.cn1s;
+  float nb, cn1;
+  if (UNI) {  // every entry of each weight vector equal (build_uniform_coeffs), cn1 a scalar
+    nb = cf.w2l * pE;
+    nb = nb + cf.w2s * pW;
+    nb = nb + cf.w3l * pN;
+    nb = nb + cf.w3s * pS;
+    nb = nb + cf.w4l * pT;
+    nb = nb + cf.w4s * pB;
+    cn1 = cf.cn1s;
+  } else {
+    nb = cf.cn2l[i - 1] * pE;
+    nb = nb + cf.cn2s[i - 1] * pW;
+    nb = nb + cf.cn3l[j - 1] * pN;
+    nb = nb + cf.cn3s[j - 1] * pS;
+    nb = nb + cf.cn4l[k - 1] * pT;
+    nb = nb + cf.cn4s[k - 1] * pB;
+    cn1 = cf.cn1 ? cf.cn1[((long long)(i - 1) * g.jm + (j - 1)) * g.km + (k - 1)] : cf.cn1s;
+  }
   pc_out = pc;
   // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
   return om * (cn1 * (nb - rhs[c]) - pc);
 }
 
 // One red-black colour pass, in place (sor.py:194-200).  Thread x enumerates
-// the colour's cells along k: k = 1 + ((i0 + j0 + nrd) & 1) + 2 t.
-template <int POL>
+// the colour's cells along k: k = 1 + ((i0 + j0 + nrd) & 1) + 2 t.  UNI uses
+// the scalar weights and 32-bit indices (grids below 2^31 cells).
+template <int POL, bool UNI>
 __global__ void __launch_bounds__(RB_BX* RB_BY) k_sor_rb(Geo g, float* __restrict__ p, const float* __restrict__ rhs,
                                                          SorC cf, float om, int nrd, int y_stored,
                                                          double* __restrict__ partials) {
@@ -78,10 +91,16 @@ __global__ void __launch_bounds__(RB_BX* RB_BY) k_sor_rb(Geo g, float* __restric
     const int ig0 = i + g.ioff - 1;
     const int k = 1 + ((ig0 + (j - 1) + nrd) & 1) + 2 * t;
     if (k <= g.km) {
-      const long long c = cidx(g, i, j, k);
-      float pc;
-      const float rel = sor_point<POL>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
-      p[c] = pc + rel;
+      float pc, rel;
+      if (UNI) {
+        const int c = i * (int)g.si + j * g.sj + k;
+        rel = sor_point<POL, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
+        p[c] = pc + rel;
+      } else {
+        const long long c = cidx(g, i, j, k);
+        rel = sor_point<POL>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
+        p[c] = pc + rel;
+      }
       acc = (double)rel * (double)rel;
     }
   }
@@ -197,8 +216,14 @@ void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, fl
     dim3 gy((g.km + 127) / 128, g.im);
     k_refresh_y<<<gy, 128, 0, st>>>(g, p);
   }
-  if (policy == 1) k_sor_rb<1><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, y_stored, partials);
-  else k_sor_rb<0><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, 0, partials);
+  const bool uni = cf.uni && !cf.cn1 && (long long)(g.im + 3) * g.si < (1LL << 31);
+  if (policy == 1) {
+    if (uni) k_sor_rb<1, true><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, y_stored, partials);
+    else k_sor_rb<1, false><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, y_stored, partials);
+  } else {
+    if (uni) k_sor_rb<0, true><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, 0, partials);
+    else k_sor_rb<0, false><<<grid, block, 0, st>>>(g, p, rhs, cf, om, nrd, 0, partials);
+  }
 }
 
 void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rhs, const SorC& cf, float om,
