@@ -22,7 +22,8 @@ from . import les as _les
 from . import sor as _sor
 
 LES_FUNCS = ("step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf", "les_viscosity",
-             "strain_magnitude", "adam", "divergence", "press")
+             "strain_magnitude", "adam", "divergence", "press", "les_main")
+CLI_FUNCS = ("les_main",)  # gmcf_mini.cli binds les_main at import (cli.py:23)
 SOR_FUNCS = ("solve_pressure", "redblack_iteration", "twinned_sweep")
 
 _saved: dict = {}
@@ -33,7 +34,13 @@ def install(les_module=None, sor_module=None) -> None:
     implementations (idempotent)."""
     lm = les_module or importlib.import_module("gmcf_mini.les")
     sm = sor_module or importlib.import_module("gmcf_mini.sor")
-    for mod, names, impl in ((lm, LES_FUNCS, _les), (sm, SOR_FUNCS, _sor)):
+    mods = [(lm, LES_FUNCS, _les), (sm, SOR_FUNCS, _sor)]
+    if les_module is None:
+        try:
+            mods.append((importlib.import_module("gmcf_mini.cli"), CLI_FUNCS, _les))
+        except ImportError:
+            pass
+    for mod, names, impl in mods:
         for n in names:
             key = (mod.__name__, n)
             if key not in _saved:

@@ -1,0 +1,59 @@
+"""GMCF field dumps straight from the device state.
+
+Format (the reference's, dump.py:1-39): the 4 bytes ``GMCF``, the three
+dimensions as little-endian uint32, then the field as row-major
+little-endian float32; written to a temporary name and renamed, so a failed
+run leaves the complete file or nothing.  ``write_state`` downloads each field
+once (pitched D2H of the Python-visible array) and writes it; the files are
+byte-identical to the reference's ``dump.write_field`` of the same array.
+"""
+
+from __future__ import annotations
+
+import os
+from pathlib import Path
+
+import numpy as np
+
+MAGIC = b"GMCF"
+
+
+def _atomic(path: Path, chunks) -> None:
+    tmp = path.with_name(path.name + ".tmp")
+    with open(tmp, "wb") as f:
+        for c in chunks:
+            f.write(c)
+    os.replace(tmp, path)
+
+
+def write_field(path, arr: np.ndarray) -> None:
+    path = Path(path)
+    if arr.ndim != 3:
+        raise ValueError(f"field dumps are 3-D, got shape {arr.shape}")
+    head = MAGIC + np.asarray(arr.shape, dtype="<u4").tobytes()
+    body = np.ascontiguousarray(arr, dtype="<f4")
+    _atomic(path, (head, memoryview(body).cast("B")))
+
+
+def read_field(path) -> np.ndarray:
+    raw = Path(path).read_bytes()
+    if raw[:4] != MAGIC:
+        raise ValueError(f"{path}: bad magic {raw[:4]!r}")
+    dims = tuple(int(d) for d in np.frombuffer(raw[4:16], dtype="<u4"))
+    data = np.frombuffer(raw[16:], dtype="<f4")
+    if data.size != int(np.prod(dims)):
+        raise ValueError(f"{path}: payload size {data.size} != dims {dims}")
+    return data.reshape(dims).copy()
+
+
+def write_state(state, out_dir, names=("u", "v", "w", "p")) -> list:
+    """Dump fields of a (device) FlowState as ``<name>.gmcf`` files, as the
+    reference's les-standalone and coupled modes do (cli.py:187-198, 210-211)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    paths = []
+    for n in names:
+        p = out / f"{n}.gmcf"
+        write_field(p, getattr(state, n))
+        paths.append(p)
+    return paths

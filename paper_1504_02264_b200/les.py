@@ -30,7 +30,7 @@ from .sor import PressureHalo, build_uniform_coeffs
 __all__ = [
     "FlowState", "step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf",
     "strain_magnitude", "les_viscosity", "adam", "divergence", "press", "_pressure_halo",
-    "STAGES",
+    "STAGES", "run_steps", "les_main",
 ]
 
 STAGES = N.STAGE_NAMES
@@ -427,3 +427,66 @@ def run_steps(state, inflow, n_steps: int, n_iter: int = 50, scheme: Scheme = Sc
         err.step = done.value
         raise err
     return done.value
+
+
+def les_main(tile, model_id: int, flow, peers, n_steps: int, interval_microsteps: int, dt_microsteps: int = 1,
+             data_id=None, sor_iters: int = 50, scheme: Scheme = Scheme.REDBLACK, record: dict | None = None,
+             coupling_module=None):
+    """The coupled LES loop (les.py:419-470) with the flow resident on the GPU.
+
+    Same protocol as the reference -- sync every step, request a profile at
+    coupled boundaries, interpolate at (t - interval) once two profiles exist
+    (coupling.py:168-270, 366-388) -- but the state is uploaded once, every
+    step is one CUDA-graph replay with the step's inflow (km x 3 floats) as
+    its only host input, and the fields are copied back into ``flow`` when the
+    loop ends (also when a stage fails: ``flow`` then holds the end of the
+    failing step, the error names the reference stage).  ``coupling_module``
+    defaults to ``gmcf_mini.coupling``.
+    """
+    if coupling_module is None:
+        import importlib
+
+        coupling_module = importlib.import_module("gmcf_mini.coupling")
+    cp = coupling_module
+    if data_id is None:
+        data_id = cp.WIND_PROFILE_DATA_ID
+    finished_status = cp.SyncStatus.PEER_FINISHED
+    dev, target = _resolve(flow)
+    state = cp.init(tile, model_id, peers, dt_microsteps, interval_microsteps)
+    steps_done = 0
+    interval_idx = 0
+    first_interp = None
+    boundaries: list = []
+    try:
+        for _ in range(n_steps):
+            if cp.sync(state) is finished_status:
+                break
+            t = state.current_time
+            if t % interval_microsteps == 0:
+                got = cp.pre_exchange(state, data_id)
+                if got is finished_status:
+                    break
+                interval_idx += 1
+                boundaries.append({"interval": interval_idx, "time": t, "steps_before": steps_done})
+            if state.series.can_interpolate:
+                inflow = cp.interpolate_profile(state.series, t - interval_microsteps)
+                if first_interp is None:
+                    first_interp = interval_idx
+            else:
+                inflow = state.series.next
+            step(dev, inflow, n_iter=sor_iters, scheme=scheme)
+            steps_done += 1
+            cp.advance_step(state)
+    finally:
+        if target is not None:
+            for n in _STAGE_FIELDS:
+                dev._dev_newer.add(n)
+            _writeback(dev, target, _STAGE_FIELDS)
+    cp.finished(state)
+    cp.await_peer_fins(state)
+    if record is not None:
+        record["steps"] = steps_done
+        record["first_interpolation_interval"] = first_interp
+        record["boundaries"] = boundaries
+        record["profiles_received"] = state.series.count_received
+    return state
