@@ -176,6 +176,70 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
   return acc;
 }
 
+// Flat walk for the boundary phase: item w = (c - c0) * KT + t goes to thread
+// w % nth, so a warp's lanes take consecutive slots of one column (rarely
+// two): the shared loads are conflict free and the publish stores of a
+// warp are consecutive words (coalesced).  Incremental (c, t) decode.
+template <bool PRESS>
+__device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
+                                              const int4* __restrict__ pubcol, unsigned long long* X,
+                                              unsigned tag, int c0, int c1, int KT, int nrd, int KK, int CW, int sI,
+                                              int km) {
+  double acc = 0.0;
+  const int nth = RES_THREADS;
+  int c = c0 + (int)threadIdx.x / KT, t = (int)threadIdx.x - ((int)threadIdx.x / KT) * KT;
+  const int dq = nth / KT, dr = nth - (nth / KT) * KT;
+  const int kk4 = CW;
+  while (c < c1) {
+    const unsigned ci = coltab[c];
+    const int cb = (int)(ci & CB_MASK);
+    const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
+    const int k = 2 * t + 2 - kp;
+    if (k <= km) {
+      const int sl = t + 1 - kp;
+      const int s = cb + sl;
+      const float* Sc = S + nrd * KK;
+      const float* So = S + (1 - nrd) * KK;
+      const float pc = Sc[s];
+      const float pE = So[s + sI];
+      float pW = So[s - sI];
+      const float pN = So[s + kk4];
+      const float pS = So[s - kk4];
+      const float pT = So[cb + t + 1];
+      float pB = So[cb + t];
+      const float r = Sc[s + 2 * KK];
+      if (PRESS) {
+        if (ci & (1u << 29)) pW = pc;  // physical west: p[0] -> p[1]
+        if (k == 1) pB = pc;            // bottom: p[.,.,0] -> p[.,.,1]
+      }
+      // sor.py:164-171: E, W, N, S, T, B summed left to right
+      float nb = a.w2l * pE;
+      nb = nb + a.w2s * pW;
+      nb = nb + a.w3l * pN;
+      nb = nb + a.w3s * pS;
+      nb = nb + a.w4l * pT;
+      nb = nb + a.w4s * pB;
+      // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+      const float rel = a.om * (a.cn1 * (nb - r) - pc);
+      const float np = pc + rel;
+      S[nrd * KK + s] = np;
+      const int4 pub = pubcol[c];
+      if (pub.x >= 0) st_ll(X + pub.x + sl, np, tag);
+      if (pub.y >= 0) st_ll(X + pub.y + sl, np, tag);
+      if (pub.z >= 0) st_ll(X + pub.z + sl, np, tag);
+      if (pub.w >= 0) st_ll(X + pub.w + sl, np, tag);
+      acc += (double)rel * (double)rel;
+    }
+    t += dr;
+    c += dq;
+    if (t >= KT) {
+      t -= KT;
+      ++c;
+    }
+  }
+  return acc;
+}
+
 // All runs of this thread in columns [c0, c1): the columns are cut into nseg
 // runs of L cells and run u = g * (c1 - c0) + (c - c0) goes to thread
 // u % nth.  Column-fastest numbering puts a warp's lanes in consecutive
@@ -411,8 +475,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)(n + 2);
     double acc = 0.0;
-    if (!(a.debug & 2)) acc = update_phase<PRESS, true>(a, S, coltab, pubcol, X, tag, 0, nbnd, nseg_b, L_b, KT, nrd, KK, CW,
-                                           sI, km);
+    if (!(a.debug & 2)) acc = update_flat<PRESS>(a, S, coltab, pubcol, X, tag, 0, nbnd, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[4 * n + 2] = gtimer();
     if (!(a.debug & 2)) acc += update_phase<PRESS, false>(a, S, coltab, pubcol, X, tag, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW,
                                       sI, km);
