@@ -1,14 +1,18 @@
-# Round evidence: tests, bench line, press-only lines, ncu launch list and full captures.
+# Round evidence: tests, bench line, reference arm, press-only lines, ncu launch list
+# and full captures, resident-solver phase trace.  Outputs under gpurun_out/ev/.
 set -x
 mkdir -p gpurun_out/ev
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/ev/gpu.txt
 timeout 600 python -m pytest tests -q -m gpu > gpurun_out/ev/pytest_gpu.txt 2>&1; tail -3 gpurun_out/ev/pytest_gpu.txt
 timeout 900 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.err; cat gpurun_out/ev/bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ev/bench_ref.json 2>&1; tail -1 gpurun_out/ev/bench_ref.json
-for path in 2 3 1; do timeout 300 python scripts/bench_press.py 150 150 90 --path $path --halo stored >> gpurun_out/ev/press.jsonl; done
-for path in 3 1; do timeout 300 python scripts/bench_press.py 512 512 90 --path $path --halo stored --reps 3 >> gpurun_out/ev/press.jsonl; done
+rm -f gpurun_out/ev/press.jsonl
+for path in 2 1 3; do timeout 300 python scripts/bench_press.py 150 150 90 --path $path >> gpurun_out/ev/press.jsonl; done
+for path in 1 3; do timeout 300 python scripts/bench_press.py 512 512 90 --path $path --reps 3 >> gpurun_out/ev/press.jsonl; done
+LESB_SOR_MARCH=1 timeout 300 python scripts/bench_press.py 512 512 90 --path 3 --reps 3 >> gpurun_out/ev/press.jsonl
 cat gpurun_out/ev/press.jsonl
+python scripts/res_trace.py > gpurun_out/ev/res_trace.txt 2>&1; cat gpurun_out/ev/res_trace.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/ev/launches.csv python bench.py --steps 6 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_resident|k_fused_rhs|k_velnw_bondv1" -s 3 -c 3 -o gpurun_out/ev/step_full python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/ev/ncu_step.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_rbfused" -s 4 -c 1 -o gpurun_out/ev/fused512_full python scripts/bench_press.py 512 512 90 --path 3 --reps 1 --n-iter 4 > gpurun_out/ev/ncu_f512.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_rb" -s 8 -c 2 -o gpurun_out/ev/rb512_full python scripts/bench_press.py 512 512 90 --path 1 --reps 1 --n-iter 4 > gpurun_out/ev/ncu_rb512.log 2>&1
 ls -la gpurun_out/ev
