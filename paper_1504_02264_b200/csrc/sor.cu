@@ -26,8 +26,16 @@
 
 namespace lesb {
 
-constexpr int RB_BX = 32, RB_BY = 8;       // x: colour index along k, y: j
-constexpr int RB_NW = RB_BX * RB_BY / 32;
+constexpr int RB_NT = 256;  // threads per colour-pass block: x = colour cells of a column, y = j
+constexpr int RB_NW = RB_NT / 32;
+
+// Block shape of a colour pass: x spans the colour's cells of a column (so a
+// warp runs on into the next j row instead of idling), y the rows.
+static inline void rb_shape(const Geo& g, int* bx, int* by) {
+  const int kh = (g.km + 1) / 2;
+  *bx = kh < RB_NT ? kh : RB_NT;
+  *by = RB_NT / *bx;
+}
 
 template <int POL, bool UNI = false, typename IDX = long long>
 __device__ __forceinline__ float sor_point(const Geo& g, const float* __restrict__ p, const float* __restrict__ rhs,
@@ -79,12 +87,12 @@ __device__ __forceinline__ float sor_point(const Geo& g, const float* __restrict
 // the colour's cells along k: k = 1 + ((i0 + j0 + nrd) & 1) + 2 t.  UNI uses
 // the scalar weights and 32-bit indices (grids below 2^31 cells).
 template <int POL, bool UNI>
-__global__ void __launch_bounds__(RB_BX* RB_BY) k_sor_rb(Geo g, float* __restrict__ p, const float* __restrict__ rhs,
+__global__ void __launch_bounds__(RB_NT) k_sor_rb(Geo g, float* __restrict__ p, const float* __restrict__ rhs,
                                                          SorC cf, float om, int nrd, int y_stored,
                                                          double* __restrict__ partials) {
   __shared__ double red[RB_NW];
-  const int t = blockIdx.x * RB_BX + threadIdx.x;
-  const int j = blockIdx.y * RB_BY + threadIdx.y + 1;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
   const int i = blockIdx.z + 1;
   double acc = 0.0;
   if (j <= g.jm) {
@@ -104,9 +112,17 @@ __global__ void __launch_bounds__(RB_BX* RB_BY) k_sor_rb(Geo g, float* __restric
       acc = (double)rel * (double)rel;
     }
   }
-  const double s = block_sum<RB_NW>(acc, red);
-  if (threadIdx.x == 0 && threadIdx.y == 0)
-    partials[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+  // fixed-order block reduction over the block's (possibly partial) warps
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  const int ltid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  if ((ltid & 31) == 0) red[ltid >> 5] = acc;
+  __syncthreads();
+  if (ltid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < nw; ++w) sum += red[w];
+    partials[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = sum;
+  }
 }
 
 // One twinned (Jacobi) sweep: read src everywhere, write the interior of dst
@@ -200,7 +216,9 @@ __global__ void k_reduce_res(const double* __restrict__ partials, int nblk, doub
 // ---------------------------------------------------------------------------
 int sor_blocks_rb(const Geo& g) {
   const int kh = (g.km + 1) / 2;
-  return ((kh + RB_BX - 1) / RB_BX) * ((g.jm + RB_BY - 1) / RB_BY) * g.im;
+  int bx, by;
+  rb_shape(g, &bx, &by);
+  return ((kh + bx - 1) / bx) * ((g.jm + by - 1) / by) * g.im;
 }
 int sor_blocks_tw(const Geo& g) {
   return ((g.km + TW_BX - 1) / TW_BX) * ((g.jm + TW_BY - 1) / TW_BY) * g.im;
@@ -209,8 +227,10 @@ int sor_blocks_tw(const Geo& g) {
 void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, float om, int nrd, int policy,
                     double* partials, cudaStream_t st) {
   const int kh = (g.km + 1) / 2;
-  dim3 grid((kh + RB_BX - 1) / RB_BX, (g.jm + RB_BY - 1) / RB_BY, g.im);
-  dim3 block(RB_BX, RB_BY);
+  int bx, by;
+  rb_shape(g, &bx, &by);
+  dim3 grid((kh + bx - 1) / bx, (g.jm + by - 1) / by, g.im);
+  dim3 block(bx, by);
   const int y_stored = (policy == 1 && (g.jm & 1)) ? 1 : 0;
   if (y_stored) {
     dim3 gy((g.km + 127) / 128, g.im);
