@@ -13,7 +13,8 @@ import threading
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblesb200.so")
+# LESB_LIB: an alternative build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("LESB_LIB") or os.path.join(PKG, "liblesb200.so")
 
 LESB_U, LESB_V, LESB_W, LESB_P, LESB_MASK, LESB_FGH, LESB_FGH_OLD, LESB_RHS = range(8)
 LESB_REDBLACK, LESB_TWINNED = 0, 1

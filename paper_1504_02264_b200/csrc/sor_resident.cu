@@ -51,6 +51,7 @@ namespace lesb {
 
 constexpr int RES_THREADS = 512;
 constexpr int RES_WARPS = RES_THREADS / 32;
+constexpr int NST = 6;   // LESB_RES_TRACE stamps per pass
 constexpr int RCVB = 6;  // face values each thread has in flight while receiving
 
 struct ResPlan {
@@ -78,7 +79,7 @@ struct ResArgs {
   unsigned* pflags;  // stage flag word (F_PRESS) or nullptr
   unsigned* err;     // set when a neighbour wait times out
   int debug;         // timing experiments only (LESB_RES_DEBUG): 1 no waits, 2 no updates, 4 no receive
-  unsigned long long* trace;  // LESB_RES_TRACE: [ntiles][2 n_iter][4] %globaltimer stamps, or nullptr
+  unsigned long long* trace;  // LESB_RES_TRACE: [ntiles][2 n_iter][NST] %globaltimer stamps, or nullptr
 };
 
 // Face exchange in the "LL" style: every published value travels with the
@@ -87,11 +88,11 @@ struct ResArgs {
 // value -- no fences, counters or flag round trips.
 __device__ __forceinline__ void st_ll(unsigned long long* a, float v, unsigned tag) {
   const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
 }
 __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a) {
   unsigned long long w;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
   return w;
 }
 
@@ -100,6 +101,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+
+__host__ __device__ __forceinline__ int row_pad(int cw) { return (32 - ((4 * cw) & 31)) & 31; }
 
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
 
@@ -117,9 +120,8 @@ constexpr unsigned CB_MASK = 0x0FFFFFFFu;
 // addresses of consecutive cells differ by one slot, and the bottom neighbour
 // of cell t+1 is the top neighbour of cell t, so a run costs 7 shared loads
 // and 1 store per cell with no per-cell index arithmetic.
-template <bool PRESS, bool PUBLISH>
-__device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigned ci, int4 pub,
-                                             unsigned long long* X, unsigned tag, int t0, int t1, int nrd,
+template <bool PRESS>
+__device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigned ci, int t0, int t1, int nrd,
                                              int KK, int CW, int sI, int km) {
   const int cb = (int)(ci & CB_MASK);
   const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
@@ -134,8 +136,52 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
   double acc = 0.0;
   if (t0 >= t1) return acc;
   float pB = tb[0];
-  int sl = t0 + 1 - kp;
-  for (int t = t0; t < t1; ++t) {
+  int t = t0;
+  // Groups of RU cells: every load of the group is issued before the first
+  // store (the colour-nrd stores never alias the other-colour and rhs loads,
+  // which the compiler cannot prove), so RU point updates overlap.
+  constexpr int RU = 4;
+  for (; t + RU <= t1; t += RU) {
+    float pc[RU], pE[RU], pW[RU], pN[RU], pS[RU], pT[RU], r[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      pc[u] = cur[u];
+      pE[u] = oth[sI + u];
+      pW[u] = oth[-sI + u];
+      pN[u] = oth[CW + u];
+      pS[u] = oth[-CW + u];
+      pT[u] = tb[1 + u];
+      r[u] = rr[u];
+    }
+    double d[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      float pb = u == 0 ? pB : pT[u - 1];
+      float pw = pW[u];
+      if (PRESS) {
+        if (wphys) pw = pc[u];                          // physical west: p[0] -> p[1]
+        if (u == 0 && t == 0 && kp == 1) pb = pc[u];    // bottom: p[.,.,0] -> p[.,.,1]
+      }
+      // sor.py:164-171: E, W, N, S, T, B summed left to right
+      float nb = a.w2l * pE[u];
+      nb = nb + a.w2s * pw;
+      nb = nb + a.w3l * pN[u];
+      nb = nb + a.w3s * pS[u];
+      nb = nb + a.w4l * pT[u];
+      nb = nb + a.w4s * pb;
+      // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+      const float rel = a.om * (a.cn1 * (nb - r[u]) - pc[u]);
+      cur[u] = pc[u] + rel;
+      d[u] = (double)rel * (double)rel;
+    }
+    acc += (d[0] + d[1]) + (d[2] + d[3]);
+    pB = pT[RU - 1];
+    cur += RU;
+    oth += RU;
+    tb += RU;
+    rr += RU;
+  }
+  for (; t < t1; ++t) {
     const float pc = *cur;
     const float pE = oth[sI];
     float pW = oth[-sI];
@@ -145,33 +191,23 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
     const float r = *rr;
     float pb = pB;
     if (PRESS) {
-      if (wphys) pW = pc;                   // physical west: p[0] -> p[1]
-      if (t == 0 && kp == 1) pb = pc;       // bottom: p[.,.,0] -> p[.,.,1]
+      if (wphys) pW = pc;
+      if (t == 0 && kp == 1) pb = pc;
     }
-    // sor.py:164-171: E, W, N, S, T, B summed left to right
     float nb = a.w2l * pE;
     nb = nb + a.w2s * pW;
     nb = nb + a.w3l * pN;
     nb = nb + a.w3s * pS;
     nb = nb + a.w4l * pT;
     nb = nb + a.w4s * pb;
-    // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
     const float rel = a.om * (a.cn1 * (nb - r) - pc);
-    const float np = pc + rel;
-    *cur = np;
-    if (PUBLISH) {
-      if (pub.x >= 0) st_ll(X + pub.x + sl, np, tag);
-      if (pub.y >= 0) st_ll(X + pub.y + sl, np, tag);
-      if (pub.z >= 0) st_ll(X + pub.z + sl, np, tag);
-      if (pub.w >= 0) st_ll(X + pub.w + sl, np, tag);
-    }
+    *cur = pc + rel;
     acc += (double)rel * (double)rel;
     pB = pT;
     ++cur;
     ++oth;
     ++tb;
     ++rr;
-    ++sl;
   }
   return acc;
 }
@@ -245,21 +281,18 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
 // u % nth.  Column-fastest numbering puts a warp's lanes in consecutive
 // columns at the same slot offset; with the odd column stride their shared
 // addresses fall in distinct banks.
-template <bool PRESS, bool PUBLISH>
+template <bool PRESS>
 __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
-                                               const int4* __restrict__ pubcol, unsigned long long* X,
-                                               unsigned tag, int c0, int c1, int nseg, int L, int KT, int nrd,
-                                               int KK, int CW, int sI, int km) {
+                                               int c0, int c1, int nseg, int L, int KT, int nrd, int KK, int CW,
+                                               int sI, int km) {
   double acc = 0.0;
-  const int nunits = (c1 - c0) * nseg;
   const int ncc = c1 - c0;
+  const int nunits = ncc * nseg;
   for (int u = threadIdx.x; u < nunits; u += RES_THREADS) {
     const int g = u / ncc, cc = u - g * ncc;
-    const int c = c0 + cc;
     const int t0 = g * L;
     const int t1 = min(t0 + L, KT);
-    const int4 pub = PUBLISH ? pubcol[c] : make_int4(-1, -1, -1, -1);
-    acc += update_run<PRESS, PUBLISH>(a, S, coltab[c], pub, X, tag, t0, t1, nrd, KK, CW, sI, km);
+    acc += update_run<PRESS>(a, S, coltab[c0 + cc], t0, t1, nrd, KK, CW, sI, km);
   }
   return acc;
 }
@@ -280,18 +313,22 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   const int TI = I1 - I0, TJ = J1 - J0;
   const int KK = pl.kk, KT = pl.kt, km = g.km;
   const int CW = 4 * KK + 1;                 // floats per column (odd: lanes in different columns spread over banks)
-  const int sI = (TJ + 2) * CW;              // column stride along i
-  const int ncol_h_max = (pl.ti_max + 2) * (pl.tj_max + 2);
-  float* S = smem;                           // [ti+2][tj+2][4][KK]
+  // column stride along i, padded so that sI = (TJ - 2) CW (mod 32): the
+  // interior columns then sit at CW * (ordinal) + const modulo the 32 banks,
+  // and a warp's lanes on 32 consecutive interior columns never conflict
+  const int PADI = row_pad(CW);
+  const int sI = (TJ + 2) * CW + PADI;
+  float* S = smem;                           // [ti+2][sI]: columns of [4][KK] (+1), rows padded
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
-  unsigned* coltab = reinterpret_cast<unsigned*>(smem + (((long long)ncol_h_max * CW + 3) & ~3LL));   // [TI*TJ]
+  const long long s_floats = (long long)(pl.ti_max + 2) * ((pl.tj_max + 2) * CW + PADI);
+  unsigned* coltab = reinterpret_cast<unsigned*>(smem + ((s_floats + 3) & ~3LL));   // [TI*TJ]
   int4* pubcol = reinterpret_cast<int4*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
   int4* rcvtab = pubcol + pl.ti_max * pl.tj_max;                                      // [2TI+2TJ]
   const long long fstride = (long long)fmax * KK;
   const long long tstride = 4 * fstride;     // words per tile in one face buffer
   const long long bstride = tstride * ntiles;  // words per face buffer
 
-  auto colbase = [&](int li, int lj) { return (li * (TJ + 2) + lj) * CW; };
+  auto colbase = [&](int li, int lj) { return li * sI + lj * CW; };
 
   // neighbour tiles (-1: physical boundary with a fixed / remapped halo)
   int nbr[4];
@@ -403,83 +440,121 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   }
 
   // runs: every thread gets about one boundary run and one interior run
-  const int nseg_b = max(1, min(KT, nbnd > 0 ? nth / nbnd : 1));
-  const int L_b = (KT + nseg_b - 1) / nseg_b;
   const int nint = ncol - nbnd;
   const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
   const int L_i = (KT + nseg_i - 1) / nseg_i;
-  // receive walk over (face column q, slot sl)
+  // receive walk over (face column q, slot sl): item w = tid + nth u.  The
+  // first RCVB items of every thread keep their descriptors in registers for
+  // the whole solve (source word, halo slot, wrap bit, and per colour whether
+  // the slot holds a published cell); any further items are decoded per pass.
   const int nrcv = nfc * KK;
-  const int rq0 = tid / KK, rs0 = tid - rq0 * KK;
-  const int rdq = nth / KK, rdr = nth - rdq * KK;
+  int roff[RCVB], rdst[RCVB];
+  unsigned rwrap = 0, rval0 = 0, rval1 = 0;
+#pragma unroll
+  for (int u = 0; u < RCVB; ++u) {
+    const int w = tid + nth * u;
+    const int q = w / KK, sl = w - (w / KK) * KK;
+    roff[u] = 0;
+    rdst[u] = -1;
+    if (q < nfc) {
+      const int4 e = rcvtab[q];
+      if (e.y >= 0) {
+        roff[u] = e.y + sl;
+        rdst[u] = e.x + sl;
+        if (e.z) rwrap |= 1u << u;
+        // only slots holding cells of the source colour were published
+        // (bit u of rval<c>: the slot is valid in the passes of colour c)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int kps = (((1 - c) ^ e.z) + e.w + 1) & 1;
+          const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
+          if (valid) (c ? rval1 : rval0) |= 1u << u;
+        }
+      }
+    }
+  }
   bool timed_out = false;
 
-  unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * 4 : nullptr;
+  unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * NST : nullptr;
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
-    if (tr && tid == 0) tr[4 * n + 0] = gtimer();
+    if (tr && tid == 0) tr[NST * n + 0] = gtimer();
     // Receive the neighbours' faces into this tile's colour-(1-nrd) halo
     // slots: pass n-1's publish, or pass n-2's across an odd-jm periodic wrap.
     // Those slots were last read in pass n-2, which every thread finished
     // before the barrier of pass n-1, so no barrier is needed before this.
-    {
+    if (!(a.debug & 4)) {
       const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
       const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
       float* Sd = S + (1 - nrd) * KK;
-      int q = rq0, sl = rs0;
-      for (int w0 = 0; w0 < ((a.debug & 4) ? 0 : nrcv); w0 += RCVB * nth) {
-        const unsigned long long* src[RCVB];
-        unsigned want[RCVB];
-        int dst[RCVB];
-        unsigned long long v[RCVB];
+      const unsigned vm = nrd ? rval1 : rval0;
+      unsigned long long v[RCVB];
+#pragma unroll
+      for (int u = 0; u < RCVB; ++u)
+        if ((vm >> u) & 1u) v[u] = ld_ll((((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u]);
+#pragma unroll
+      for (int u = 0; u < RCVB; ++u) {
+        if (!((vm >> u) & 1u)) continue;
+        const bool w2 = (rwrap >> u) & 1u;
+        const unsigned want = w2 ? t2 : t1;
+        unsigned spins = 0;
+        while ((unsigned)(v[u] >> 32) != want && !timed_out && !(a.debug & 1)) {
+          if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
+            atomicOr(a.err, 1u);
+            timed_out = true;
+          }
+          v[u] = ld_ll((w2 ? XB2 : XB1) + roff[u]);
+        }
+        Sd[rdst[u]] = __uint_as_float((unsigned)v[u]);
+      }
+      // items beyond the register-held ones (large tiles / deep columns)
+      for (int w0 = RCVB * nth; w0 < nrcv; w0 += RCVB * nth) {
+        int off[RCVB], dst[RCVB];
+        unsigned wrapm = 0;
 #pragma unroll
         for (int u = 0; u < RCVB; ++u) {
           dst[u] = -1;
+          const int w = w0 + tid + nth * u;
+          const int q = w / KK, sl = w - (w / KK) * KK;
           if (q < nfc) {
             const int4 e = rcvtab[q];
-            // only slots holding cells of the source colour were published
             const int kps = (((1 - nrd) ^ e.z) + e.w + 1) & 1;
             const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
             if (e.y >= 0 && valid) {
-              src[u] = (e.z ? XB2 : XB1) + e.y + sl;
-              want[u] = e.z ? t2 : t1;
+              off[u] = e.y + sl;
               dst[u] = e.x + sl;
-              v[u] = ld_ll(src[u]);
+              if (e.z) wrapm |= 1u << u;
+              v[u] = ld_ll((e.z ? XB2 : XB1) + off[u]);
             }
-          }
-          sl += rdr;
-          q += rdq;
-          if (sl >= KK) {
-            sl -= KK;
-            ++q;
           }
         }
 #pragma unroll
         for (int u = 0; u < RCVB; ++u) {
           if (dst[u] < 0) continue;
+          const bool w2 = (wrapm >> u) & 1u;
+          const unsigned want = w2 ? t2 : t1;
           unsigned spins = 0;
-          while ((unsigned)(v[u] >> 32) != want[u] && !timed_out && !(a.debug & 1)) {
-            if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
+          while ((unsigned)(v[u] >> 32) != want && !timed_out && !(a.debug & 1)) {
+            if (++spins > (1u << 24)) {
               atomicOr(a.err, 1u);
               timed_out = true;
             }
-            v[u] = ld_ll(src[u]);
+            v[u] = ld_ll((w2 ? XB2 : XB1) + off[u]);
           }
           Sd[dst[u]] = __uint_as_float((unsigned)v[u]);
         }
       }
     }
     __syncthreads();
-    if (tr && tid == 0) tr[4 * n + 1] = gtimer();
+    if (tr && tid == 0) tr[NST * n + 1] = gtimer();
     unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)(n + 2);
     double acc = 0.0;
     if (!(a.debug & 2)) acc = update_flat<PRESS>(a, S, coltab, pubcol, X, tag, 0, nbnd, KT, nrd, KK, CW, sI, km);
-    if (tr && tid == 0) tr[4 * n + 2] = gtimer();
-    if (!(a.debug & 2)) acc += update_phase<PRESS, false>(a, S, coltab, pubcol, X, tag, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW,
-                                      sI, km);
-    if (tr && tid == 0) tr[4 * n + 3] = gtimer();
+    if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
+    if (!(a.debug & 2)) acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW, sI, km);
+    if (tr && tid == 0) tr[NST * n + 5] = gtimer();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
     if (lane == 0) a.partials[((long long)n * ntiles + tile) * RES_WARPS + warp] = acc;
@@ -547,7 +622,8 @@ static int g_num_sms = -1;
 static int g_max_smem = -1;
 
 static size_t plan_smem(int tim, int tjm, int kk) {
-  const size_t arrays = 4ull * ((((size_t)4 * kk + 1) * (tim + 2) * (tjm + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
+  const int cw = 4 * kk + 1;
+  const size_t arrays = 4ull * ((((size_t)cw * (tjm + 2) + row_pad(cw)) * (tim + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
   const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
   const size_t pubcol = 16ull * tim * tjm;
   const size_t rcvtab = 16ull * 2 * (tim + tjm);
@@ -644,7 +720,7 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
   a.debug = dbg;
   a.trace = nullptr;
   static const bool trace = getenv("LESB_RES_TRACE") != nullptr;
-  const size_t tneed = (size_t)ntiles * 2 * n_iter * 4;
+  const size_t tneed = (size_t)ntiles * 2 * n_iter * NST;
   if (trace) {
     if (g_tcap < tneed) {
       if (g_tbuf) cudaFree(g_tbuf);
@@ -662,8 +738,9 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
 }  // namespace lesb
 
 // Debug only (not in the public header): copy the last traced launch's
-// stamps ([tile][pass][4]: before receive, after receive barrier, after
-// boundary runs, after interior runs) to host; returns the word count.
+// stamps ([tile][pass][NST]: before receive, after receive barrier, after
+// the boundary phase (three copies), after interior runs) to host; returns
+// the word count.
 extern "C" long long lesb_debug_resident_trace(unsigned long long* host, long long cap) {
   using namespace lesb;
   if (!g_tbuf || !host) return 0;

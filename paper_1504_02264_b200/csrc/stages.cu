@@ -556,8 +556,11 @@ void launch_fused_rhs(const Geo& g, const Spac& s, const float* ub, const float*
                       const float* mask, float* fgh, float* fgh_old, float* ua, float* va, float* wa, float* rhs,
                       float vn, float dt, int do_les, const float* csd2f, float csd2s, unsigned* flags,
                       cudaStream_t st) {
-  dim3 gr, bl;
-  box_launch(g.km + 2, g.jm + 2, g.im + 2, gr, bl);
+  // one-warp-wide blocks, 4 rows: measured fastest on B200 for 150x150x90
+  // (64.0 us vs 73.7 us for 96x2 blocks; the kernel is latency bound and
+  // small blocks retire without waiting on a slow sibling warp)
+  const dim3 bl(32, 4, 1);
+  const dim3 gr((g.km + 2 + 31) / 32, (g.jm + 2 + 3) / 4, g.im + 2);
   if (s.p2)
     k_fused_rhs<true><<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
                                          csd2f, csd2s, flags);

@@ -17,27 +17,23 @@ lib = N.load()
 res = np.zeros(50)
 for _ in range(3):
     N.check(lib.lesb_press(h.h, 50, 0, 1.7, N.dptr(res)), "press")
-buf = np.zeros(200 * 100 * 4, np.uint64)
+NST = 6
+buf = np.zeros(200 * 100 * NST, np.uint64)
 fn = lib.lesb_debug_resident_trace
 fn.restype = ctypes.c_longlong
 n = fn(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), buf.size)
-nt = n // (100 * 4)
-t = buf[:n].reshape(nt, 100, 4).astype(np.int64)
-t0 = t[:, 0, 0].min()
-t = t - t0
-print("tiles", nt, "kernel span (first recv -> last interior end) us", (t[:, -1, 3].max()) / 1e3)
-d_recv = (t[:, :, 1] - t[:, :, 0]) / 1e3
-d_bnd = (t[:, :, 2] - t[:, :, 1]) / 1e3
-d_int = (t[:, :, 3] - t[:, :, 2]) / 1e3
-gap = (t[:, 1:, 0] - t[:, :-1, 3]) / 1e3
-print("per-pass means over tiles/passes (us): recv+barrier %.2f  boundary %.2f  interior %.2f  end->next %.2f" %
-      (d_recv[:, 2:].mean(), d_bnd[:, 2:].mean(), d_int[:, 2:].mean(), gap[:, 2:].mean()))
+nt = n // (100 * NST)
+t = buf[:n].reshape(nt, 100, NST).astype(np.int64)
+t = t - t[:, 0, 0].min()
+names = ["recv+barrier", "boundary", "barrier", "publish", "interior"]
+d = [(t[:, :, q + 1] - t[:, :, q]) / 1e3 for q in range(NST - 1)]
+gap = (t[:, 1:, 0] - t[:, :-1, NST - 1]) / 1e3
+print("tiles", nt, "kernel span us", t[:, -1, NST - 1].max() / 1e3)
+print("per-pass means over tiles/passes (us): " + "  ".join(
+    "%s %.2f" % (nm, x[:, 2:].mean()) for nm, x in zip(names, d)) + "  end->next %.2f" % gap[:, 2:].mean())
 per_pass = (t[:, 2:, 0].max(0)[1:] - t[:, 2:, 0].max(0)[:-1]) / 1e3
 print("pass period (max start over tiles) us: mean %.2f min %.2f max %.2f" % (per_pass.mean(), per_pass.min(), per_pass.max()))
-print("tile 0 passes 10-14 (recv, bnd, int):", [(round(a, 2), round(b, 2), round(c, 2)) for a, b, c in zip(d_recv[0, 10:15], d_bnd[0, 10:15], d_int[0, 10:15])])
 print("start skew across tiles at pass 50 (us): %.2f" % ((t[:, 50, 0].max() - t[:, 50, 0].min()) / 1e3))
-comp = (d_bnd + d_int)[:, 2:].mean(1)
+comp = sum(d[1:])[:, 2:].mean(1)
 order = np.argsort(comp)
-print("per-tile compute (bnd+int) us: min %.2f median %.2f max %.2f" % (comp.min(), np.median(comp), comp.max()))
-print("slowest tiles:", [(int(t), round(float(comp[t]), 2)) for t in order[-6:]])
-print("fastest tiles:", [(int(t), round(float(comp[t]), 2)) for t in order[:4]])
+print("per-tile work after receive (us): min %.2f median %.2f max %.2f" % (comp.min(), np.median(comp), comp.max()))
