@@ -218,7 +218,7 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
 // warp are consecutive words (coalesced).  Incremental (c, t) decode.
 template <bool PRESS>
 __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
-                                              const int4* __restrict__ pubcol, unsigned long long* X,
+                                              const int2* __restrict__ pubcol, unsigned long long* X,
                                               unsigned tag, int c0, int c1, int KT, int nrd, int KK, int CW, int sI,
                                               int km) {
   double acc = 0.0;
@@ -259,11 +259,9 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
       const float rel = a.om * (a.cn1 * (nb - r) - pc);
       const float np = pc + rel;
       S[nrd * KK + s] = np;
-      const int4 pub = pubcol[c];
-      if (pub.x >= 0) st_ll(X + pub.x + sl, np, tag);
-      if (pub.y >= 0) st_ll(X + pub.y + sl, np, tag);
-      if (pub.z >= 0) st_ll(X + pub.z + sl, np, tag);
-      if (pub.w >= 0) st_ll(X + pub.w + sl, np, tag);
+      const int2 pub = pubcol[c];  // a column lies on at most two faces
+      if (pub.x >= 0) st_ll(X + (pub.x + sl), np, tag);
+      if (pub.y >= 0) st_ll(X + (pub.y + sl), np, tag);
       acc += (double)rel * (double)rel;
     }
     t += dr;
@@ -322,8 +320,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
   const long long s_floats = (long long)(pl.ti_max + 2) * ((pl.tj_max + 2) * CW + PADI);
   unsigned* coltab = reinterpret_cast<unsigned*>(smem + ((s_floats + 3) & ~3LL));   // [TI*TJ]
-  int4* pubcol = reinterpret_cast<int4*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
-  int4* rcvtab = pubcol + pl.ti_max * pl.tj_max;                                      // [2TI+2TJ]
+  int2* pubcol = reinterpret_cast<int2*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
+  int4* rcvtab = reinterpret_cast<int4*>(pubcol + ((pl.ti_max * pl.tj_max + 1) & ~1));  // [2TI+2TJ]
   const long long fstride = (long long)fmax * KK;
   const long long tstride = 4 * fstride;     // words per tile in one face buffer
   const long long bstride = tstride * ntiles;  // words per face buffer
@@ -363,10 +361,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     const int i = I0 - 1 + li, j = J0 - 1 + lj;
     coltab[c] = (unsigned)colbase(li, lj) | ((unsigned)((i + j) & 1) << 28) |
                 ((wtile && li == 1) ? (1u << 29) : 0u);
-    pubcol[c] = make_int4(li == 1 ? (int)(0 * fstride + (lj - 1) * KK) : -1,
-                          li == TI ? (int)(1 * fstride + (lj - 1) * KK) : -1,
-                          lj == 1 ? (int)(2 * fstride + (li - 1) * KK) : -1,
-                          lj == TJ ? (int)(3 * fstride + (li - 1) * KK) : -1);
+    // face words of the column: west / east face (x), south / north face (y)
+    const int fx = li == 1 ? (int)(0 * fstride + (lj - 1) * KK) : (li == TI ? (int)(1 * fstride + (lj - 1) * KK) : -1);
+    const int fy = lj == 1 ? (int)(2 * fstride + (li - 1) * KK) : (lj == TJ ? (int)(3 * fstride + (li - 1) * KK) : -1);
+    // (tiles are at least 2 x 2 columns, so no column lies on more faces)
+    pubcol[c] = fx >= 0 ? make_int2(fx, fy) : make_int2(fy, -1);
   }
   const int nfc = 2 * TJ + 2 * TI;
   for (int q = tid; q < nfc; q += nth) {
@@ -429,14 +428,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   for (int w = tid; w < nbnd * 2 * KK; w += nth) {
     const int c = w / (2 * KK), r = w - c * 2 * KK;
     const int col_c = r >= KK ? 1 : 0, sl = r - col_c * KK;
-    const int4 f = pubcol[c];
+    const int2 f = pubcol[c];
     const float v = S[(coltab[c] & CB_MASK) + r];
     unsigned long long* X = a.xbuf + (2 + col_c) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)col_c;
     if (f.x >= 0) st_ll(X + f.x + sl, v, tag);
     if (f.y >= 0) st_ll(X + f.y + sl, v, tag);
-    if (f.z >= 0) st_ll(X + f.z + sl, v, tag);
-    if (f.w >= 0) st_ll(X + f.w + sl, v, tag);
   }
 
   // runs: every thread gets about one boundary run and one interior run
@@ -625,7 +622,7 @@ static size_t plan_smem(int tim, int tjm, int kk) {
   const int cw = 4 * kk + 1;
   const size_t arrays = 4ull * ((((size_t)cw * (tjm + 2) + row_pad(cw)) * (tim + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
   const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
-  const size_t pubcol = 16ull * tim * tjm;
+  const size_t pubcol = 8ull * ((tim * tjm + 1) & ~1);
   const size_t rcvtab = 16ull * 2 * (tim + tjm);
   return arrays + coltab + pubcol + rcvtab;
 }
@@ -641,8 +638,9 @@ ResPlan plan_resident(const Geo& g, int device) {
   pl.kk = ((g.km + 1) >> 1) + 1;
   pl.kt = (g.km + 1) >> 1;
   size_t best = (size_t)-1;
-  for (int ni = 1; ni <= g.im && ni <= g_num_sms; ++ni) {
-    for (int nj = 1; nj <= g.jm && ni * nj <= g_num_sms; ++nj) {
+  // tiles of at least 2 x 2 columns: a column then lies on at most two faces
+  for (int ni = 1; 2 * ni <= g.im && ni <= g_num_sms; ++ni) {
+    for (int nj = 1; 2 * nj <= g.jm && ni * nj <= g_num_sms; ++nj) {
       const int tim = (g.im + ni - 1) / ni, tjm = (g.jm + nj - 1) / nj;
       const size_t smem = plan_smem(tim, tjm, pl.kk);
       if (smem > (size_t)g_max_smem - 2048) continue;
