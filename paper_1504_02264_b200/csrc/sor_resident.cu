@@ -90,6 +90,9 @@ __device__ __forceinline__ void st_ll(unsigned long long* a, float v, unsigned t
   const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
 }
+__device__ __forceinline__ void st_ll_word(unsigned long long* a, unsigned long long w) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
+}
 __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a) {
   unsigned long long w;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
@@ -225,7 +228,9 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
   const int nth = RES_THREADS;
   int c = c0 + (int)threadIdx.x / KT, t = (int)threadIdx.x - ((int)threadIdx.x / KT) * KT;
   const int dq = nth / KT, dr = nth - (nth / KT) * KT;
-  const int kk4 = CW;
+  float* Sc = S + nrd * KK;
+  const float* So = S + (1 - nrd) * KK;
+  const unsigned long long tagw = (unsigned long long)tag << 32;
   while (c < c1) {
     const unsigned ci = coltab[c];
     const int cb = (int)(ci & CB_MASK);
@@ -233,17 +238,16 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
     const int k = 2 * t + 2 - kp;
     if (k <= km) {
       const int sl = t + 1 - kp;
-      const int s = cb + sl;
-      const float* Sc = S + nrd * KK;
-      const float* So = S + (1 - nrd) * KK;
-      const float pc = Sc[s];
-      const float pE = So[s + sI];
-      float pW = So[s - sI];
-      const float pN = So[s + kk4];
-      const float pS = So[s - kk4];
-      const float pT = So[cb + t + 1];
-      float pB = So[cb + t];
-      const float r = Sc[s + 2 * KK];
+      const float* o = So + (cb + sl);  // other colour, same k
+      float* ce = Sc + (cb + sl);       // centre
+      const float pc = ce[0];
+      const float pE = o[sI];
+      float pW = o[-sI];
+      const float pN = o[CW];
+      const float pS = o[-CW];
+      const float pT = o[kp];           // slot t + 1
+      float pB = o[kp - 1];             // slot t
+      const float r = ce[2 * KK];
       if (PRESS) {
         if (ci & (1u << 29)) pW = pc;  // physical west: p[0] -> p[1]
         if (k == 1) pB = pc;            // bottom: p[.,.,0] -> p[.,.,1]
@@ -258,10 +262,11 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
       // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
       const float rel = a.om * (a.cn1 * (nb - r) - pc);
       const float np = pc + rel;
-      S[nrd * KK + s] = np;
+      ce[0] = np;
       const int2 pub = pubcol[c];  // a column lies on at most two faces
-      if (pub.x >= 0) st_ll(X + (pub.x + sl), np, tag);
-      if (pub.y >= 0) st_ll(X + (pub.y + sl), np, tag);
+      const unsigned long long w = tagw | __float_as_uint(np);
+      if (pub.x >= 0) st_ll_word(X + (unsigned)(pub.x + sl), w);
+      if (pub.y >= 0) st_ll_word(X + (unsigned)(pub.y + sl), w);
       acc += (double)rel * (double)rel;
     }
     t += dr;
