@@ -74,6 +74,7 @@ __global__ void k_velnw_inplace(Geo g, Spac s, float* __restrict__ u, float* __r
 struct BondSrc {
   int kind;  // 0 zero, 1 inflow, 2 interior cell
   int kk;
+  int ii, jj;  // source cell (ii, jj, kk) when kind == 2
   long long src;
 };
 
@@ -85,6 +86,8 @@ __device__ __forceinline__ bool bond_source(const Geo& g, int comp, int i, int j
   if (i == 0) { b.kind = 1; b.kk = kk; return true; }
   int ii = i == g.im + 1 ? g.im : i;
   b.kind = 2;
+  b.ii = ii;
+  b.jj = jj;
   b.src = cidx(g, ii, jj, kk);
   return true;
 }
@@ -144,12 +147,9 @@ __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const
         } else if (b.kind == 1) {
           val = inflow[m * g.km + b.kk - 1];
         } else {
-          int si_ = (int)(b.src / g.si);
-          int sj_ = (int)((b.src % g.si) / g.sj);
-          int sk_ = (int)(b.src % g.sj);
-          val = m == 0 ? velnw_u<P2>(g, s, u, p, fgh, dt, b.src, si_)
-              : (m == 1 ? velnw_v<P2>(g, s, v, p, fgh, dt, b.src, sj_)
-                        : velnw_w<P2>(g, s, w, p, fgh, dt, b.src, sk_));
+          val = m == 0 ? velnw_u<P2>(g, s, u, p, fgh, dt, b.src, b.ii)
+              : (m == 1 ? velnw_v<P2>(g, s, v, p, fgh, dt, b.src, b.jj)
+                        : velnw_w<P2>(g, s, w, p, fgh, dt, b.src, b.kk));
         }
         if (!finite32(val)) bits |= F_BONDV1;
         out[m][c] = val;
