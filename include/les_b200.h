@@ -187,6 +187,22 @@ int lesb_twinned_sweep(int im, int jm, int km, const float* src, float* dst, con
  * low, 2 high), pressure after every colour pass / sweep and after the final
  * halo.  Results equal the single-domain step bitwise. */
 /* ncclGetUniqueId into out (>= 128 bytes); returns the id size. */
+/* ---- boundary-range launch geometry (sor.py:312-349; the paper's gid -> face map) ----
+ * lesb_boundary_decode: device decode of gids [gid0, gid0 + n) exactly as
+ *   map_boundary_gid (sor.py:319-338): face 0 YZ (j, k), 1 ZX (k, i), 2 XY (j, i),
+ *   -1 PADDING (c0 = c1 = -1); host output arrays of n ints.
+ * lesb_boundary_audit: cli.py:286-320 on the device -- one launch of blocks of
+ *   nthreads threads x nunits gids over padded_range (sor.py:341-349);
+ *   stats[8] = {boundary_range, padded_range, in-range gids decoded to padding,
+ *   padding gids escaping the guard, points covered once, points covered more
+ *   than once, points never covered, smallest violating gid or -1}.
+ * lesb_boundp_faces: the pressure halo refresh (les.py:341-355) of the
+ *   face-interior halo cells (the cells the SOR stencil reads), one launch over
+ *   the boundary range; edges and corners are left as they are. */
+int lesb_boundary_decode(int ip, int jp, int kp, long long gid0, long long n, int* face, int* c0, int* c1);
+int lesb_boundary_audit(int ip, int jp, int kp, int nthreads, int nunits, long long* stats);
+int lesb_boundp_faces(lesb_handle h);
+
 int lesb_nccl_unique_id(void* out, int nbytes);
 /* One process per GPU: rank r's neighbours are r-1 (west) and r+1 (east). */
 int lesb_link_nccl(lesb_handle h, const void* unique_id, int nranks, int rank);

@@ -90,6 +90,9 @@ _SIGS = {
                                           C.c_float, C.c_int, DP, C.c_int]),
     "lesb_twinned_sweep": (C.c_int, [C.c_int, C.c_int, C.c_int, FP, FP, FP, C.POINTER(lesb_coeffs),
                                      C.c_float, DP, C.c_int]),
+    "lesb_boundary_decode": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_longlong, IP, IP, IP]),
+    "lesb_boundary_audit": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
+    "lesb_boundp_faces": (C.c_int, [C.c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -1171,3 +1171,62 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
 }
 
 }  // extern "C"
+
+/* ---------------------------------------------------------------------------
+ * Boundary-range launch geometry (sor.py:312-349, cli.py:286-320)
+ * ------------------------------------------------------------------------- */
+int lesb_boundary_decode(int ip, int jp, int kp, long long gid0, long long n, int* face, int* c0, int* c1) {
+  using namespace lesb;
+  if (ip < 1 || jp < 1 || kp < 1) return fail(LESB_E_ARG, "ip, jp, kp must be >= 1");
+  if (gid0 < 0) return fail(LESB_E_ARG, "gid must be >= 0");
+  if (n < 0 || (n > 0 && (!face || !c0 || !c1))) return fail(LESB_E_ARG, "output arrays are required");
+  if (n == 0) return LESB_OK;
+  int* d = nullptr;
+  CK(cudaMalloc(&d, 3 * n * sizeof(int)));
+  cudaError_t e = launch_boundary_decode(gid0, n, ip, jp, kp, d, d + n, d + 2 * n, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(face, d, n * sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(c0, d + n, n * sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(c1, d + 2 * n, n * sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("boundary decode: ") + cudaGetErrorString(e));
+  return LESB_OK;
+}
+
+int lesb_boundary_audit(int ip, int jp, int kp, int nthreads, int nunits, long long* stats) {
+  using namespace lesb;
+  if (ip < 1 || jp < 1 || kp < 1) return fail(LESB_E_ARG, "ip, jp, kp must be >= 1");
+  if (nthreads < 1 || nunits < 1) return fail(LESB_E_ARG, "nthreads and nunits must be >= 1");
+  if (nthreads > 1024) return fail(LESB_E_ARG, "nthreads must be <= 1024 (one launch block)");
+  if (!stats) return fail(LESB_E_ARG, "stats array is required");
+  const long long br = boundary_range(ip, jp, kp);
+  const long long pr = padded_range(br, nthreads, nunits);
+  unsigned* hits = nullptr;
+  unsigned long long* buf = nullptr;  // stats[5], first[3]
+  CK(cudaMalloc(&hits, br * sizeof(unsigned)));
+  cudaError_t e = cudaMalloc(&buf, 8 * sizeof(unsigned long long));
+  unsigned long long hb[8] = {0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull};
+  if (e == cudaSuccess) e = cudaMemset(hits, 0, br * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemcpy(buf, hb, sizeof hb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_boundary_audit(ip, jp, kp, nthreads, nunits, hits, buf, buf + 5, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(hb, buf, sizeof hb, cudaMemcpyDeviceToHost);
+  cudaFree(hits);
+  cudaFree(buf);
+  if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("boundary audit: ") + cudaGetErrorString(e));
+  stats[0] = br;
+  stats[1] = pr;
+  stats[2] = (long long)hb[0];  // in-range gids decoded to padding
+  stats[3] = (long long)hb[1];  // padding gids that escaped the guard
+  stats[4] = (long long)hb[2];  // points covered exactly once
+  stats[5] = (long long)hb[3];  // points covered more than once
+  stats[6] = (long long)hb[4];  // points never covered
+  const unsigned long long f0 = hb[5] < hb[6] ? hb[5] : hb[6];
+  stats[7] = f0 == ~0ull ? -1 : (long long)f0;  // smallest violating gid
+  return LESB_OK;
+}
+
+int lesb_boundp_faces(lesb_handle h) {
+  STAGE_PROLOGUE();
+  launch_boundp_faces(h->g, h->p, h->st);
+  STAGE_EPILOGUE();
+}
+

@@ -91,4 +91,13 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
                                 int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
                                 double* res, unsigned* pflags, unsigned* err, cudaStream_t st);
 
+// boundary.cu: boundary-range launch geometry (sor.py:312-349)
+long long boundary_range(int ip, int jp, int kp);
+long long padded_range(long long range, int nthreads, int nunits);
+cudaError_t launch_boundary_decode(long long gid0, long long n, int ip, int jp, int kp, int* face, int* c0, int* c1,
+                                   cudaStream_t st);
+cudaError_t launch_boundary_audit(int ip, int jp, int kp, int nthreads, int nunits, unsigned* hits,
+                                  unsigned long long* stats, unsigned long long* first, cudaStream_t st);
+void launch_boundp_faces(const Geo& g, float* p, cudaStream_t st);
+
 }  // namespace lesb

@@ -23,7 +23,9 @@ from . import sor as _sor
 
 LES_FUNCS = ("step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf", "les_viscosity",
              "strain_magnitude", "adam", "divergence", "press", "les_main")
-CLI_FUNCS = ("les_main",)  # gmcf_mini.cli binds les_main at import (cli.py:23)
+CLI_FUNCS = ("les_main", "run_boundary_audit")  # cli.py:23 binds les_main at import
+# cli.main dispatches through the _RUNNERS table built at import (cli.py:323-328)
+CLI_RUNNERS = {"boundary-audit": "run_boundary_audit"}
 SOR_FUNCS = ("solve_pressure", "redblack_iteration", "twinned_sweep")
 
 _saved: dict = {}
@@ -42,16 +44,29 @@ def install(les_module=None, sor_module=None) -> None:
             pass
     for mod, names, impl in mods:
         for n in names:
+            if not hasattr(mod, n):
+                continue
             key = (mod.__name__, n)
             if key not in _saved:
                 _saved[key] = (mod, getattr(mod, n))
             setattr(mod, n, getattr(impl, n))
+        runners = getattr(mod, "_RUNNERS", None) if names is CLI_FUNCS else None
+        if isinstance(runners, dict):
+            for mode, fn in CLI_RUNNERS.items():
+                if mode in runners:
+                    key = (mod.__name__, "_RUNNERS:" + mode)
+                    if key not in _saved:
+                        _saved[key] = (runners, runners[mode])
+                    runners[mode] = getattr(impl, fn)
 
 
 def uninstall() -> None:
     """Restore the reference implementations."""
     for (_modname, n), (mod, fn) in list(_saved.items()):
-        setattr(mod, n, fn)
+        if n.startswith("_RUNNERS:"):
+            mod[n[len("_RUNNERS:"):]] = fn
+        else:
+            setattr(mod, n, fn)
     _saved.clear()
 
 

@@ -35,6 +35,14 @@ def write_field(path, arr: np.ndarray) -> None:
     _atomic(path, (head, memoryview(body).cast("B")))
 
 
+def write_json(path, obj) -> None:
+    """JSON summary, indent 2 and a trailing newline, written atomically
+    (dump.py:54-56)."""
+    import json
+
+    _atomic(Path(path), ((json.dumps(obj, indent=2) + "\n").encode(),))
+
+
 def read_field(path) -> np.ndarray:
     raw = Path(path).read_bytes()
     if raw[:4] != MAGIC:

@@ -30,7 +30,7 @@ from .sor import PressureHalo, build_uniform_coeffs
 __all__ = [
     "FlowState", "step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf",
     "strain_magnitude", "les_viscosity", "adam", "divergence", "press", "_pressure_halo",
-    "STAGES", "run_steps", "les_main",
+    "STAGES", "run_steps", "les_main", "refresh_pressure_faces", "run_boundary_audit",
 ]
 
 STAGES = N.STAGE_NAMES
@@ -248,6 +248,15 @@ def _stage(state, fn_name, writes, *args):
 def velnw(state) -> None:
     """u += dt*(fgh - grad p), staggered, faces 0..N (les.py:218-241)."""
     _stage(state, "lesb_velnw", ("u", "v", "w"))
+
+
+def refresh_pressure_faces(state) -> None:
+    """The pressure halo refresh (les.py:341-355) on the face-interior halo
+    cells -- the cells the SOR stencil reads -- launched over the paper's
+    boundary-range geometry (sor.py:312-349): one GPU launch of
+    padded_range(boundary_range(im, jm, km), 256, 1) threads, each decoding
+    its gid to a face point.  Edges and corners are left unchanged."""
+    _stage(state, "lesb_boundp_faces", ("p",))
 
 
 def _inflow_arrays(inflow, km):
@@ -490,3 +499,47 @@ def les_main(tile, model_id: int, flow, peers, n_steps: int, interval_microsteps
         record["boundaries"] = boundaries
         record["profiles_received"] = state.series.count_received
     return state
+
+
+def run_boundary_audit(cfg, out_dir):
+    """``boundary-audit`` mode (cli.py:286-320) with the decode on the GPU.
+
+    The reference walks every gid of the padded range through
+    map_boundary_gid in Python; here one launch of blocks of cfg.nthreads
+    threads x cfg.nunits gids decodes them all (sor.boundary_audit) and the
+    checks are the reference's: every boundary point covered exactly once,
+    no in-range gid in the padding branch, no padding gid escaping the guard.
+    Prints the reference's line and writes the same summary.json."""
+    from pathlib import Path
+
+    from . import dump as _dump
+    from . import sor as _sor
+    from .reftypes import GmcfError
+
+    ip, jp, kp = cfg.im, cfg.jm, cfg.km
+    st = _sor.boundary_audit(ip, jp, kp, cfg.nthreads, cfg.nunits)
+    br, pr = st["boundary_range"], st["padded_range"]
+    if st["range_gids_in_padding"]:
+        raise GmcfError(f"coverage violation: gid {st['first_violation']} mapped to padding inside the range")
+    if st["covered_more"]:
+        raise GmcfError(f"coverage violation: {st['covered_more']} boundary points hit more than once")
+    expected = jp * kp + kp * ip + jp * ip
+    if st["covered_once"] != expected:
+        raise GmcfError(f"coverage violation: {st['covered_once']} points covered, expected {expected}")
+    if st["padding_escapes"]:
+        raise GmcfError(f"padding violation: gid {st['first_violation']} escaped the guard")
+    print(
+        f"boundary audit ok: domain=({ip},{jp},{kp}) m={cfg.nthreads * cfg.nunits} "
+        f"covered={br} padding={pr - br}",
+        flush=True,
+    )
+    summary = {
+        "mode": "boundary-audit",
+        "domain": [ip, jp, kp],
+        "boundary_range": br,
+        "padded_range": pr,
+        "padding_gids": pr - br,
+    }
+    _dump.write_json(Path(out_dir) / "summary.json", summary)
+    return summary
+

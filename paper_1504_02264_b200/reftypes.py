@@ -12,8 +12,8 @@ from __future__ import annotations
 
 try:  # pragma: no cover - depends on the environment
     from gmcf_mini.coupling import WindProfile  # type: ignore
-    from gmcf_mini.errors import NumericsError  # type: ignore
-    from gmcf_mini.sor import Grid, Scheme, SorCoeffs  # type: ignore
+    from gmcf_mini.errors import GmcfError, NumericsError  # type: ignore
+    from gmcf_mini.sor import PADDING, BoundaryPoint, Face, Grid, Scheme, SorCoeffs  # type: ignore
 
     HAVE_REFERENCE = True
 except Exception:  # noqa: BLE001
@@ -28,7 +28,32 @@ except Exception:  # noqa: BLE001
         REDBLACK = "redblack"
         TWINNED = "twinned"
 
-    class NumericsError(Exception):  # errors.py:20-28
+    class Face(enum.Enum):  # sor.py:34-37
+        YZ = "yz"
+        ZX = "zx"
+        XY = "xy"
+
+    class _Padding:  # sor.py:40-49
+        """Sentinel for gids that fall in the padded tail of the boundary range."""
+
+        __slots__ = ()
+
+        def __repr__(self) -> str:
+            return "PADDING"
+
+    PADDING = _Padding()
+
+    @dataclass(frozen=True)
+    class BoundaryPoint:  # sor.py:52-61
+        """One boundary-face point: (j, k) on YZ, (k, i) on ZX, (j, i) on XY."""
+
+        face: Face
+        coords: tuple
+
+    class GmcfError(Exception):  # errors.py:8-9
+        pass
+
+    class NumericsError(GmcfError):  # errors.py:20-28
         """A numerical stage produced non-finite values."""
 
         def __init__(self, stage: str, detail: str = ""):
@@ -75,7 +100,7 @@ except Exception:  # noqa: BLE001
         cn4l: np.ndarray
         cn4s: np.ndarray
 
-    class ConfigError(Exception):
+    class ConfigError(GmcfError):
         pass
 
     @dataclass

@@ -14,11 +14,13 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as N
-from .reftypes import Grid, Scheme, SorCoeffs, is_redblack
+from .reftypes import PADDING, BoundaryPoint, Face, Grid, Scheme, SorCoeffs, is_redblack
 
 __all__ = [
     "Grid", "Scheme", "SorCoeffs", "build_uniform_coeffs", "make_field", "make_twinned",
     "redblack_iteration", "twinned_sweep", "solve_pressure", "PressureHalo", "halo_policy",
+    "Face", "BoundaryPoint", "PADDING", "boundary_range", "map_boundary_gid", "padded_range",
+    "boundary_decode", "boundary_audit",
 ]
 
 
@@ -170,3 +172,86 @@ def twinned_sweep(tp, rhs, c, omega, nrd: int) -> float:
             "twinned_sweep")
     tp[..., 1 - nrd] = dst
     return float(res[0])
+
+
+# ---------------------------------------------------------------------------
+# Boundary-range launch geometry (sor.py:312-349; the paper's gid -> face map)
+# ---------------------------------------------------------------------------
+def boundary_range(ip: int, jp: int, kp: int) -> int:
+    """Size of the 1-D index space enumerating the three boundary families
+    (sor.py:312-316)."""
+    if min(ip, jp, kp) < 1:
+        raise ValueError("ip, jp, kp must be >= 1")
+    return jp * kp + kp * ip + jp * ip
+
+
+def map_boundary_gid(gid: int, ip: int, jp: int, kp: int):
+    """Decode one global id into a boundary point, or PADDING past the range
+    (sor.py:319-338; host index math, as in the reference).  The device does
+    the same decode for whole launches: boundary_decode / boundary_audit."""
+    if gid < 0:
+        raise ValueError("gid must be >= 0")
+    n_yz = jp * kp
+    n_zx = kp * ip
+    if gid < n_yz:
+        return BoundaryPoint(Face.YZ, (gid % jp, gid // jp))
+    if gid < n_yz + n_zx:
+        r = gid - n_yz
+        return BoundaryPoint(Face.ZX, (r // ip, r % ip))
+    if gid < n_yz + n_zx + jp * ip:
+        r = gid - n_yz - n_zx
+        return BoundaryPoint(Face.XY, (r // ip, r % ip))
+    return PADDING
+
+
+def padded_range(range_: int, nthreads: int, nunits: int) -> int:
+    """Pad a work range up to a multiple of nthreads * nunits (sor.py:341-349)."""
+    if range_ < 0:
+        raise ValueError("range must be >= 0")
+    if nthreads < 1 or nunits < 1:
+        raise ValueError("nthreads and nunits must be >= 1")
+    m = nthreads * nunits
+    rem = range_ % m
+    return range_ if rem == 0 else range_ + (m - rem)
+
+
+_FACES = (Face.YZ, Face.ZX, Face.XY)
+
+
+def boundary_decode(ip: int, jp: int, kp: int, gid0: int = 0, n: int | None = None):
+    """Decode gids [gid0, gid0 + n) on the GPU (default: the whole boundary
+    range).  Returns (face, c0, c1) int32 arrays: face 0 YZ, 1 ZX, 2 XY, -1
+    PADDING, (c0, c1) the BoundaryPoint coords (-1 for padding)."""
+    boundary_range(ip, jp, kp)
+    if gid0 < 0:
+        raise ValueError("gid must be >= 0")
+    if n is None:
+        n = boundary_range(ip, jp, kp) - gid0
+    n = max(int(n), 0)
+    face = np.empty(n, np.int32)
+    c0 = np.empty(n, np.int32)
+    c1 = np.empty(n, np.int32)
+    ip_ = lambda a: a.ctypes.data_as(N.IP)  # noqa: E731
+    N.check(N.load().lesb_boundary_decode(ip, jp, kp, int(gid0), n, ip_(face), ip_(c0), ip_(c1)),
+            "boundary_decode")
+    return face, c0, c1
+
+
+def boundary_points(face, c0, c1) -> list:
+    """BoundaryPoint / PADDING objects of decoded arrays (for comparison with
+    map_boundary_gid)."""
+    return [PADDING if f < 0 else BoundaryPoint(_FACES[f], (int(a), int(b))) for f, a, b in zip(face, c0, c1)]
+
+
+def boundary_audit(ip: int, jp: int, kp: int, nthreads: int, nunits: int) -> dict:
+    """The boundary audit (cli.py:286-320) as one GPU launch: every gid of
+    the padded range decoded by the thread that would own it (blocks of
+    nthreads threads x nunits gids), per-point hit counts, padding guard."""
+    boundary_range(ip, jp, kp)
+    padded_range(0, nthreads, nunits)
+    st = (N.C.c_longlong * 8)()
+    N.check(N.load().lesb_boundary_audit(ip, jp, kp, nthreads, nunits, st), "boundary_audit")
+    keys = ("boundary_range", "padded_range", "range_gids_in_padding", "padding_escapes", "covered_once",
+            "covered_more", "not_covered", "first_violation")
+    return dict(zip(keys, (int(x) for x in st)))
+

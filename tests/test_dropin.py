@@ -69,3 +69,28 @@ def test_reference_pressure_halo_maps_to_press_policy(ref):
         S.halo_policy(lambda p: None, (6, 7, 5))
     with pytest.raises(ValueError):
         S.halo_policy(S.PressureHalo(grid), (6, 8, 5))
+
+
+def test_install_rebinds_cli_runners(ref):
+    """cli.main dispatches through _RUNNERS (cli.py:323-328): install() swaps
+    the boundary-audit runner for the GPU one and uninstall() restores it."""
+    cli = pytest.importorskip("gmcf_mini.cli")
+    import paper_1504_02264_b200 as P
+
+    orig_runner = cli._RUNNERS["boundary-audit"]
+    orig_fn = cli.run_boundary_audit
+    orig_main = cli.les_main
+    P.install()
+    try:
+        assert cli._RUNNERS["boundary-audit"] is P.les.run_boundary_audit
+        assert cli.run_boundary_audit is P.les.run_boundary_audit
+        assert cli.les_main is P.les.les_main
+        for mode in ("coupled", "les-standalone", "sor-bench"):
+            assert cli._RUNNERS[mode] is getattr(cli, {"coupled": "run_coupled",
+                                                       "les-standalone": "run_les_standalone",
+                                                       "sor-bench": "run_sor_bench"}[mode])
+    finally:
+        P.uninstall()
+    assert cli._RUNNERS["boundary-audit"] is orig_runner
+    assert cli.run_boundary_audit is orig_fn
+    assert cli.les_main is orig_main
