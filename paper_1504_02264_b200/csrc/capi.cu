@@ -125,6 +125,16 @@ struct lesb_domain {
   int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 colour-fused streaming
   void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
   unsigned* repoch = nullptr;  // resident solver tag epoch
+  // x-slab on NCCL ranks: the neighbour ranks' face buffers mapped through
+  // CUDA IPC (peer memory over NVLink) so the resident solver exchanges tile
+  // faces inside its one launch; peer_ready once both sides are mapped
+  void* peer_w = nullptr;
+  void* peer_e = nullptr;
+  bool peer_ready = false;
+  bool peer_tried = false;
+  // in-process slab group: face buffers sized for the group plan, shared epoch
+  void* gxbuf = nullptr;
+  unsigned* gepoch = nullptr;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool known_finite = false;
   long long n_alloc = 0;  // (im+3)*si
@@ -140,9 +150,15 @@ struct lesb_domain {
     // auto: the resident solver where the grid fits the SMs' shared memory,
     // else the unfused colour passes (fastest streaming option measured so
     // far, profiles/r1_v3_summary.md); the colour-fused kernel on request
-    const bool res = (sor_path == 0 || sor_path == 2) && xbuf != nullptr;
+    const bool whole = g.west_bc && g.east_bc && g.ioff == 0;  // one domain (not an x-slab)
+    const bool res = (sor_path == 0 || sor_path == 2) && xbuf != nullptr && (whole || peer_ready);
     const bool fz = sor_path == 3;
-    return ResidentBufs{res, device, fz ? 1 : 0, xbuf, repoch, &book_d->err};
+    ResidentBufs rb{res, device, fz ? 1 : 0, xbuf, repoch, &book_d->err};
+    if (res && !whole) {
+      rb.peer_w = peer_w;
+      rb.peer_e = peer_e;
+    }
+    return rb;
   }
   long long n_int() const { return (long long)g.im * g.jm * g.km; }
 };
@@ -184,6 +200,47 @@ void set_spacing_info(lesb_domain* h, const float* dx, const float* dy, const fl
   s.rdt = s.dtp2 ? 1.0f / h->dt : 0.f;
 }
 
+// Exchange the face-buffer IPC handles of an NCCL slab with every rank (one
+// all-gather, at the first solve: every rank takes it) and open the west /
+// east neighbours' buffers.  All ranks run the same plan (same slab shape),
+// so the ghost slots line up.  Returns false (and leaves the slab on the
+// streaming path) when any step fails, e.g. without peer access.
+void clear_graphs(lesb_domain* h);
+
+bool map_slab_peers(lesb_domain* h) {
+  const int nr = h->link.nranks, r = h->link.rank;
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, h->xbuf) != cudaSuccess) return false;
+  // the handle plus this slab's plan signature: (im, jm, km, buffer words)
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    long long im, jm, km, words;
+  } rec{mine, h->g.im, h->g.jm, h->g.km, resident_xbuf_words(h->g, h->device)};
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(Rec) * (nr + 1)) != cudaSuccess) return false;
+  std::vector<Rec> all(nr);
+  bool ok = cudaMemcpy((char*)d + sizeof(Rec) * nr, &rec, sizeof(Rec), cudaMemcpyHostToDevice) == cudaSuccess &&
+            ncclAllGather((char*)d + sizeof(Rec) * nr, d, sizeof(Rec), ncclChar, h->link.comm, h->st) == ncclSuccess &&
+            cudaStreamSynchronize(h->st) == cudaSuccess &&
+            cudaMemcpy(all.data(), d, sizeof(Rec) * nr, cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(d);
+  if (!ok) return false;
+  for (int q = 0; q < nr; ++q)
+    if (all[q].im != rec.im || all[q].jm != rec.jm || all[q].km != rec.km || all[q].words != rec.words) return false;
+  void* w = nullptr;
+  void* e = nullptr;
+  if (r > 0 && cudaIpcOpenMemHandle(&w, all[r - 1].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return false;
+  if (r < nr - 1 && cudaIpcOpenMemHandle(&e, all[r + 1].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    if (w) cudaIpcCloseMemHandle(w);
+    return false;
+  }
+  h->peer_w = w;
+  h->peer_e = e;
+  h->peer_ready = true;
+  clear_graphs(h);
+  return true;
+}
+
 int ensure_partials(lesb_domain* h, int n_iter) {
   long long need = (long long)n_iter * 2 *
                    std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_partials(h->g, h->device)),
@@ -200,6 +257,10 @@ int ensure_partials(lesb_domain* h, int n_iter) {
     CK(cudaMemset(h->xbuf, 0, xb));
     CK(cudaMalloc(&h->repoch, sizeof(unsigned)));
     CK(cudaMemset(h->repoch, 0, sizeof(unsigned)));
+  }
+  if (h->link.comm && h->xbuf && !h->peer_tried) {
+    h->peer_tried = true;
+    map_slab_peers(h);  // on failure the slab keeps the streaming colour passes
   }
   if (n_iter > h->res_cap) {
     if (h->res_d) cudaFree(h->res_d);
@@ -296,9 +357,12 @@ cudaError_t enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, b
                           unsigned* flags) {
   if (rhs_from_state) launch_divergence(h->g, h->spac(), h->u, h->v, h->w, h->rhs, h->dt, 1, h->st);
   ResidentBufs rb = h->rbufs();
-  ExchangeHook hook{h->link.comm ? nccl_p_hook : nullptr, h};
-  return enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d, flags, h->st,
-                     &hook, nullptr, &rb);
+  const bool res_slab = h->link.comm && rb.use && scheme == 0;  // resident solver exchanging through peer memory
+  ExchangeHook hook{h->link.comm && !res_slab ? nccl_p_hook : nullptr, h};
+  cudaError_t e = enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials, h->res_d,
+                              flags, h->st, &hook, nullptr, &rb);
+  if (e == cudaSuccess && res_slab) nccl_exchange(h, h->p, 1, h->st);  // inner x halo planes: the final values
+  return e;
 }
 
 // The full step: velnw+bondv1 (A -> B), velfg+feedbf+les+adam+rhs (B -> A), press.
@@ -321,11 +385,13 @@ cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omeg
   launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
                    h->vn, h->dt, h->cs != 0.0f, h->csd2, h->csd2s, flags, h->st);
   mark(2);
-  ExchangeHook hook{h->link.comm ? nccl_p_hook : nullptr, h};
   SorMarks marks{h->timing ? h->ev[3] : nullptr};
   ResidentBufs rb = h->rbufs();
+  const bool res_slab = h->link.comm && rb.use && scheme == 0;  // resident solver exchanging through peer memory
+  ExchangeHook hook{h->link.comm && !res_slab ? nccl_p_hook : nullptr, h};
   cudaError_t e = enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials,
                               h->res_d, flags, h->st, &hook, &marks, &rb);
+  if (e == cudaSuccess && res_slab) nccl_exchange(h, h->p, 1, h->st);  // inner x halo planes: the final values
   mark(4);
   return e;
 }
@@ -493,6 +559,8 @@ int lesb_destroy(lesb_handle h) {
   if (!h) return LESB_OK;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->peer_w) cudaIpcCloseMemHandle(h->peer_w);
+  if (h->peer_e) cudaIpcCloseMemHandle(h->peer_e);
   if (h->link.comm) ncclCommDestroy(h->link.comm);
   if (h->link.west) h->link.west->link.east = nullptr;
   if (h->link.east) h->link.east->link.west = nullptr;
@@ -505,6 +573,8 @@ int lesb_destroy(lesb_handle h) {
   if (h->partials) cudaFree(h->partials);
   if (h->xbuf) cudaFree(h->xbuf);
   if (h->repoch) cudaFree(h->repoch);
+  if (h->gxbuf) cudaFree(h->gxbuf);
+  if (h->gepoch) cudaFree(h->gepoch);
   if (h->res_d) cudaFree(h->res_d);
   if (h->book_d) cudaFree(h->book_d);
   if (h->res_h) cudaFreeHost(h->res_h);
@@ -1127,7 +1197,38 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
     if (scheme == LESB_TWINNED)
       CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
-  for (int it = 0; it < n_iter; ++it) {
+  // Red-black on slabs of one shape: the resident solver for the whole group
+  // in one cooperative launch, tile faces crossing slab boundaries through
+  // the neighbours' ghost slots (the in-process form of the NVLink peer path)
+  bool group_res = scheme == LESB_REDBLACK && n <= resident_group_max() &&
+                   (h0->sor_path == 0 || h0->sor_path == 2) && !std::getenv("LESB_GROUP_PASSES");
+  for (int s = 0; s < n && group_res; ++s)
+    group_res = hs[s]->g.im == h0->g.im && hs[s]->g.jm == h0->g.jm && hs[s]->g.km == h0->g.km &&
+                resident_supported(hs[s]->g, hs[s]->sorc(), hs[s]->device, resident_group_tiles(n));
+  if (group_res) {
+    for (int s = 0; s < n; ++s) {
+      lesb_domain* h = hs[s];
+      if (!h->gxbuf) {
+        const size_t xb = resident_xbuf_words(h->g, h->device, resident_group_tiles(n)) * sizeof(unsigned long long);
+        CK(cudaMalloc(&h->gxbuf, xb));
+        CK(cudaMemset(h->gxbuf, 0, xb));
+        CK(cudaMalloc(&h->gepoch, sizeof(unsigned)));
+        CK(cudaMemset(h->gepoch, 0, sizeof(unsigned)));
+      }
+    }
+    std::vector<ResidentCall> calls(n);
+    std::vector<SorC> cfs(n);
+    for (int s = 0; s < n; ++s) {
+      lesb_domain* h = hs[s];
+      cfs[s] = h->sorc();
+      calls[s] = ResidentCall{&h->g,        h->device,  h->p,        h->rhs,   &cfs[s],
+                              omega,        n_iter,     1,           h->gxbuf, h0->gepoch,
+                              h->partials,  h->res_d,   &h->book_d->flags,     &h0->book_d->err,
+                              s > 0 ? hs[s - 1]->gxbuf : nullptr, s < n - 1 ? hs[s + 1]->gxbuf : nullptr};
+    }
+    CK(launch_sor_resident_group(n, calls.data(), st));
+  }
+  for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {
       for (int s = 0; s < n; ++s) {
         lesb_domain* h = hs[s];
@@ -1148,13 +1249,27 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
   for (int s = 0; s < n; ++s) local_exchange(hs[s], &lesb_domain::p, 1, st);
   for (int s = 0; s < n; ++s) {
     lesb_domain* h = hs[s];
-    launch_reduce_res(h->partials, scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g), n_iter,
-                      h->res_d, st);
+    if (!group_res)  // (the resident solver reduces its residuals itself)
+      launch_reduce_res(h->partials, scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g), n_iter,
+                        h->res_d, st);
     CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
+  if (group_res) {  // a neighbour wait that timed out: reset the group's face buffers and report
+    unsigned e = 0;
+    CK(cudaMemcpy(&e, &h0->book_d->err, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    if (e) {
+      for (int s = 0; s < n; ++s) {
+        cudaMemset(hs[s]->gxbuf, 0, resident_xbuf_words(hs[s]->g, hs[s]->device, resident_group_tiles(n)) * 8);
+        cudaMemset(hs[s]->gepoch, 0, sizeof(unsigned));
+      }
+      cudaMemset(&h0->book_d->err, 0, sizeof(unsigned));
+      cudaDeviceSynchronize();
+      return fail(LESB_E_CUDA, "resident SOR (slab group): neighbour wait timed out");
+    }
+  }
   unsigned bits = 0;
   for (int s = 0; s < n; ++s) {
     bits |= hs[s]->book_h->flags;

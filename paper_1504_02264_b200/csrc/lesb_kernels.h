@@ -29,6 +29,8 @@ struct ResidentBufs {
   void* xbuf;        // resident_xbuf_words() 64-bit words, zero-initialised
   unsigned* epoch;   // one word, zero-initialised
   unsigned* err;
+  void* peer_w = nullptr;  // x-slab: neighbour slabs' face buffers (peer memory)
+  void* peer_e = nullptr;
 };
 
 // stages.cu
@@ -83,13 +85,33 @@ cudaError_t launch_rb_march(const Geo& g, int device, const float* pa, float* pb
                             float om, int policy, double* partials, cudaStream_t st);
 
 // sor_resident.cu
-bool resident_supported(const Geo& g, const SorC& cf, int device);
-int resident_ntiles(const Geo& g, int device);
-int resident_partials(const Geo& g, int device);  // per-pass residual partials
-long long resident_xbuf_words(const Geo& g, int device);
-cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
-                                int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
-                                double* res, unsigned* pflags, unsigned* err, cudaStream_t st);
+// max_tiles: 0 for every SM (one domain or one slab per GPU); num_SMs / n for
+// a group of n in-process slabs launched together
+bool resident_supported(const Geo& g, const SorC& cf, int device, int max_tiles = 0);
+int resident_ntiles(const Geo& g, int device, int max_tiles = 0);
+int resident_partials(const Geo& g, int device, int max_tiles = 0);  // per-pass residual partials
+long long resident_xbuf_words(const Geo& g, int device, int max_tiles = 0);
+struct ResidentCall {
+  const Geo* g;
+  int device;
+  float* p;
+  const float* rhs;
+  const SorC* cf;
+  float om;
+  int n_iter, policy;
+  void* xbuf;
+  unsigned* epoch;
+  double* partials;
+  double* res;
+  unsigned* pflags;
+  unsigned* err;
+  void* peer_w;  // x-slab neighbours' face buffers (another GPU's, mapped), or nullptr
+  void* peer_e;
+};
+cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st);
+cudaError_t launch_sor_resident_group(int n, const ResidentCall* cs, cudaStream_t st);
+int resident_group_max();
+int resident_group_tiles(int n);  // tiles per slab when n slabs share one launch
 
 // boundary.cu: boundary-range launch geometry (sor.py:312-349)
 long long boundary_range(int ip, int jp, int kp);

@@ -60,7 +60,9 @@ struct ResPlan {
   int kk;           // slots per colour column: ((km + 1) >> 1) + 1
   int kt;           // work items per column and pass: (km + 1) >> 1
   size_t smem;      // dynamic shared memory bytes
-  long long xbuf;   // floats of the face exchange buffer
+  long long fstride;  // words per face slot
+  long long bstride;  // words per ring buffer: ntiles * 4 faces + 2 * nj ghost slots
+  long long xbuf;   // words of the face exchange buffer (4 ring buffers)
   bool ok;
 };
 
@@ -72,7 +74,14 @@ struct ResArgs {
   float om, cn1;
   float w2l, w2s, w3l, w3s, w4l, w4s;
   int n_iter;
-  unsigned long long* xbuf;  // [4][ntiles][4][fmax * kk] (value, tag) words, ring of 4 passes
+  unsigned long long* xbuf;  // [4 ring][ntiles * 4 faces + 2 nj ghost slots][fstride] (value, tag) words
+  // x-slabs: the face buffers of the neighbouring slabs (same
+  // plan), or nullptr at a physical x face.  An edge tile writes its x face
+  // straight into the neighbour's ghost slot for its tj (west peer: ghost-E
+  // slot, east peer: ghost-W slot) and reads its own ghost slots; on another
+  // GPU the peer buffer is NVLink peer memory and those words use .sys scope.
+  unsigned long long* peer_w;
+  unsigned long long* peer_e;
   unsigned* epoch;   // launch counter: tags of this launch are unique across launches
   double* partials;  // [2 n_iter][ntiles][RES_WARPS] per-warp residual partials
   double* res;       // [n_iter] residual per iteration
@@ -93,6 +102,14 @@ __device__ __forceinline__ void st_ll(unsigned long long* a, float v, unsigned t
 __device__ __forceinline__ void st_ll_word(unsigned long long* a, unsigned long long w) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
 }
+__device__ __forceinline__ void st_ll_sys(unsigned long long* a, unsigned long long w) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a), "l"(w));
+}
+__device__ __forceinline__ unsigned long long ld_ll_sys(const unsigned long long* a) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
+  return w;
+}
 __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a) {
   unsigned long long w;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
@@ -110,7 +127,7 @@ __host__ __device__ __forceinline__ int row_pad(int cw) { return (32 - ((4 * cw)
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
 
 // colour of a cell: the pass nrd updates cells with colour == nrd
-// ((i-1)+(j-1)+(k-1)+nrd even, sor.py:174-178)
+// ((i-1)+(j-1)+(k-1)+nrd even, sor.py:174-178), i GLOBAL (an x-slab adds ioff)
 __device__ __forceinline__ int colour(int i, int j, int k) { return (i + j + k + 1) & 1; }
 
 // Shared-memory column layout: [p colour 0 | p colour 1 | rhs colour 0 |
@@ -118,6 +135,8 @@ __device__ __forceinline__ int colour(int i, int j, int k) { return (i + j + k +
 // operand of a point update is (column base + slot + a per-pass constant).
 // Column-table entry: column base | parity(i+j) << 28 | west-physical << 29.
 constexpr unsigned CB_MASK = 0x0FFFFFFFu;
+// publish-table flags: the face word lives in the west / east peer slab's buffer
+constexpr int PUB_RW = 1 << 30, PUB_RE = 1 << 29, PUB_OFF = PUB_RE - 1;
 
 // One run of work: colour-nrd cells t0 <= t < t1 of one column.  The
 // addresses of consecutive cells differ by one slot, and the bottom neighbour
@@ -219,11 +238,11 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
 // w % nth, so a warp's lanes take consecutive slots of one column (rarely
 // two): the shared loads are conflict free and the publish stores of a
 // warp are consecutive words (coalesced).  Incremental (c, t) decode.
-template <bool PRESS>
+template <bool PRESS, bool SLAB>
 __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
                                               const int2* __restrict__ pubcol, unsigned long long* X,
-                                              unsigned tag, int c0, int c1, int KT, int nrd, int KK, int CW, int sI,
-                                              int km) {
+                                              unsigned long long* XRw, unsigned long long* XRe, unsigned tag,
+                                              int c0, int c1, int KT, int nrd, int KK, int CW, int sI, int km) {
   double acc = 0.0;
   const int nth = RES_THREADS;
   int c = c0 + (int)threadIdx.x / KT, t = (int)threadIdx.x - ((int)threadIdx.x / KT) * KT;
@@ -265,8 +284,20 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
       ce[0] = np;
       const int2 pub = pubcol[c];  // a column lies on at most two faces
       const unsigned long long w = tagw | __float_as_uint(np);
-      if (pub.x >= 0) st_ll_word(X + (unsigned)(pub.x + sl), w);
-      if (pub.y >= 0) st_ll_word(X + (unsigned)(pub.y + sl), w);
+      if (!SLAB) {
+        if (pub.x >= 0) st_ll_word(X + (unsigned)(pub.x + sl), w);
+        if (pub.y >= 0) st_ll_word(X + (unsigned)(pub.y + sl), w);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int v = h ? pub.y : pub.x;
+          if (v < 0) continue;
+          const unsigned o = (unsigned)((v & PUB_OFF) + sl);
+          if (v & PUB_RW) st_ll_sys(XRw + o, w);
+          else if (v & PUB_RE) st_ll_sys(XRe + o, w);
+          else st_ll_word(X + o, w);
+        }
+      }
       acc += (double)rel * (double)rel;
     }
     t += dr;
@@ -300,15 +331,27 @@ __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const
   return acc;
 }
 
-template <bool PRESS>
-__global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
+// One launch: a single domain, or (SLAB) every in-process x-slab of a group
+// on one device -- block b works on tile b % tps of slab b / tps.  Across
+// GPUs each rank launches its own slab with peer_w / peer_e mapped.
+constexpr int RES_GROUP_MAX = 4;
+struct ResGroup {
+  ResArgs a[RES_GROUP_MAX];
+  int n;    // slabs in this launch
+  int tps;  // tiles per slab
+};
+
+template <bool PRESS, bool SLAB>
+__global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_constant__ ResGroup grp) {
   extern __shared__ float smem[];
   __shared__ double red[RES_WARPS];
+  const int slab = SLAB ? (int)blockIdx.x / grp.tps : 0;
+  const ResArgs& a = grp.a[slab];
   const Geo& g = a.g;
   const ResPlan& pl = a.pl;
   const int tid = threadIdx.x, nth = RES_THREADS;
   const int lane = tid & 31, warp = tid >> 5;
-  const int tile = blockIdx.x;
+  const int tile = SLAB ? (int)blockIdx.x - slab * grp.tps : (int)blockIdx.x;
   const int ntiles = pl.ni * pl.nj;
   const int ti = tile / pl.nj, tj = tile % pl.nj;
   const int I0 = tile_lo(ti, g.im, pl.ni), I1 = tile_lo(ti + 1, g.im, pl.ni);
@@ -322,21 +365,24 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   const int PADI = row_pad(CW);
   const int sI = (TJ + 2) * CW + PADI;
   float* S = smem;                           // [ti+2][sI]: columns of [4][KK] (+1), rows padded
-  const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
   const long long s_floats = (long long)(pl.ti_max + 2) * ((pl.tj_max + 2) * CW + PADI);
   unsigned* coltab = reinterpret_cast<unsigned*>(smem + ((s_floats + 3) & ~3LL));   // [TI*TJ]
   int2* pubcol = reinterpret_cast<int2*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
   int4* rcvtab = reinterpret_cast<int4*>(pubcol + ((pl.ti_max * pl.tj_max + 1) & ~1));  // [2TI+2TJ]
-  const long long fstride = (long long)fmax * KK;
+  const long long fstride = pl.fstride;
   const long long tstride = 4 * fstride;     // words per tile in one face buffer
-  const long long bstride = tstride * ntiles;  // words per face buffer
+  const long long bstride = pl.bstride;      // words per face buffer (tiles, then 2 nj ghost slots)
+  const long long ghost_w = ntiles * tstride + (long long)tj * fstride;           // this tile's ghost-W slot
+  const long long ghost_e = ntiles * tstride + (long long)(pl.nj + tj) * fstride;  // ... and ghost-E slot
 
   auto colbase = [&](int li, int lj) { return li * sI + lj * CW; };
 
-  // neighbour tiles (-1: physical boundary with a fixed / remapped halo)
+  // neighbour tiles (-1: physical boundary with a fixed / remapped halo;
+  // -2 / -3: the west / east neighbour slab, through this tile's ghost slot)
+  const bool pw = SLAB && a.peer_w != nullptr, pe = SLAB && a.peer_e != nullptr;
   int nbr[4];
-  nbr[0] = ti > 0 ? tile - pl.nj : -1;                                    // west  <- its east face (1)
-  nbr[1] = ti < pl.ni - 1 ? tile + pl.nj : -1;                            // east  <- its west face (0)
+  nbr[0] = ti > 0 ? tile - pl.nj : (pw ? -2 : -1);                        // west  <- its east face (1)
+  nbr[1] = ti < pl.ni - 1 ? tile + pl.nj : (pe ? -3 : -1);                // east  <- its west face (0)
   nbr[2] = tj > 0 ? tile - 1 : (PRESS ? ti * pl.nj + pl.nj - 1 : -1);     // south <- its north face (3)
   nbr[3] = tj < pl.nj - 1 ? tile + 1 : (PRESS ? ti * pl.nj : -1);         // north <- its south face (2)
   const int wrap_flip = g.jm & 1;  // periodic source parity differs from the slot's for odd jm
@@ -364,10 +410,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
       lj = 2 + r % (TJ - 2);
     }
     const int i = I0 - 1 + li, j = J0 - 1 + lj;
-    coltab[c] = (unsigned)colbase(li, lj) | ((unsigned)((i + j) & 1) << 28) |
+    coltab[c] = (unsigned)colbase(li, lj) | ((unsigned)((i + g.ioff + j) & 1) << 28) |
                 ((wtile && li == 1) ? (1u << 29) : 0u);
     // face words of the column: west / east face (x), south / north face (y)
-    const int fx = li == 1 ? (int)(0 * fstride + (lj - 1) * KK) : (li == TI ? (int)(1 * fstride + (lj - 1) * KK) : -1);
+    // (an x face of an edge tile goes to the neighbour slab's ghost slot)
+    const int fx = li == 1 ? ((ti == 0 && pw) ? (PUB_RW | ((lj - 1) * KK)) : (int)(0 * fstride + (lj - 1) * KK))
+                           : (li == TI ? ((ti == pl.ni - 1 && pe) ? (PUB_RE | ((lj - 1) * KK))
+                                                                  : (int)(1 * fstride + (lj - 1) * KK))
+                                       : -1);
     const int fy = lj == 1 ? (int)(2 * fstride + (li - 1) * KK) : (lj == TJ ? (int)(3 * fstride + (li - 1) * KK) : -1);
     // (tiles are at least 2 x 2 columns, so no column lies on more faces)
     pubcol[c] = fx >= 0 ? make_int2(fx, fy) : make_int2(fy, -1);
@@ -384,8 +434,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     // parity of the source column (the neighbour's cell, across the wrap for y)
     const int si_ = I0 - 1 + rli, sj0 = J0 - 1 + rlj;
     const int sj_ = sj0 == 0 ? g.jm : (sj0 == g.jm + 1 ? 1 : sj0);
-    rcvtab[q] = make_int4(colbase(rli, rlj), nbr[f] < 0 ? -1 : (int)(nbr[f] * tstride + (f ^ 1) * fstride + m * KK),
-                          wrap ? wrap_flip : 0, (si_ + sj_) & 1);
+    // (halo column, source word, wrap flip | ghost << 1, source parity)
+    const int nf = nbr[f];
+    const long long src_off = nf >= 0 ? nf * tstride + (f ^ 1) * fstride + m * KK
+                              : nf == -2 ? ghost_w + m * KK
+                              : nf == -3 ? ghost_e + m * KK
+                                         : -1;
+    rcvtab[q] = make_int4(colbase(rli, rlj), (int)src_off, (wrap ? wrap_flip : 0) | (nf < -1 ? 2 : 0),
+                          (si_ + g.ioff + sj_) & 1);
   }
 
   // ---- load tile columns, rhs and halo columns from global memory (warp per
@@ -400,14 +456,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     if (ih && jh) continue;  // corner columns are never read
     const int i = I0 - 1 + li, j = J0 - 1 + lj;
     const int jj = j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j);
-    const bool xphys = ih && (i == 0 || i == g.im + 1);
+    const bool xphys = ih && ((i == 0 && g.west_bc) || (i == g.im + 1 && g.east_bc));
     // stored halo / neighbour tile's initial value, or (press) the periodic y
     // halo's pre-pass snapshot of its source
     const float* src = a.p + cidx(g, i, PRESS ? jj : j, 0);
     const float* rsrc = a.rhs + cidx(g, i, j, 0);
     const bool inner = !ih && !jh;
     const int cb = colbase(li, lj);
-    const int c0 = colour(i, j, 0);
+    const int c0 = colour(i + g.ioff, j, 0);
     for (int k = lane; k <= km + 1; k += 32) {
       const bool kh = k == 0 || k == km + 1;
       // press: top / east are 0; bottom / west are remapped at read time
@@ -437,8 +493,18 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     const float v = S[(coltab[c] & CB_MASK) + r];
     unsigned long long* X = a.xbuf + (2 + col_c) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)col_c;
-    if (f.x >= 0) st_ll(X + f.x + sl, v, tag);
-    if (f.y >= 0) st_ll(X + f.y + sl, v, tag);
+    const unsigned long long word = ((unsigned long long)tag << 32) | __float_as_uint(v);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = h ? f.y : f.x;
+      if (o < 0) continue;
+      if (SLAB && (o & PUB_RW))
+        st_ll_sys(a.peer_w + (2 + col_c) * bstride + ghost_e + (o & PUB_OFF) + sl, word);
+      else if (SLAB && (o & PUB_RE))
+        st_ll_sys(a.peer_e + (2 + col_c) * bstride + ghost_w + (o & PUB_OFF) + sl, word);
+      else
+        st_ll_word(X + o + sl, word);
+    }
   }
 
   // runs: every thread gets about one boundary run and one interior run
@@ -451,7 +517,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
   // the slot holds a published cell); any further items are decoded per pass.
   const int nrcv = nfc * KK;
   int roff[RCVB], rdst[RCVB];
-  unsigned rwrap = 0, rval0 = 0, rval1 = 0;
+  unsigned rwrap = 0, rsys = 0, rval0 = 0, rval1 = 0;
 #pragma unroll
   for (int u = 0; u < RCVB; ++u) {
     const int w = tid + nth * u;
@@ -463,12 +529,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
       if (e.y >= 0) {
         roff[u] = e.y + sl;
         rdst[u] = e.x + sl;
-        if (e.z) rwrap |= 1u << u;
+        if (e.z & 1) rwrap |= 1u << u;
+        if (e.z & 2) rsys |= 1u << u;  // a ghost slot, written by a neighbour slab
         // only slots holding cells of the source colour were published
         // (bit u of rval<c>: the slot is valid in the passes of colour c)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int kps = (((1 - c) ^ e.z) + e.w + 1) & 1;
+          const int kps = (((1 - c) ^ (e.z & 1)) + e.w + 1) & 1;
           const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
           if (valid) (c ? rval1 : rval0) |= 1u << u;
         }
@@ -494,7 +561,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
       unsigned long long v[RCVB];
 #pragma unroll
       for (int u = 0; u < RCVB; ++u)
-        if ((vm >> u) & 1u) v[u] = ld_ll((((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u]);
+        if ((vm >> u) & 1u) {
+          const unsigned long long* src = (((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u];
+          v[u] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
+        }
 #pragma unroll
       for (int u = 0; u < RCVB; ++u) {
         if (!((vm >> u) & 1u)) continue;
@@ -506,14 +576,15 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
             atomicOr(a.err, 1u);
             timed_out = true;
           }
-          v[u] = ld_ll((w2 ? XB2 : XB1) + roff[u]);
+          const unsigned long long* src = (w2 ? XB2 : XB1) + roff[u];
+          v[u] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
         }
         Sd[rdst[u]] = __uint_as_float((unsigned)v[u]);
       }
       // items beyond the register-held ones (large tiles / deep columns)
       for (int w0 = RCVB * nth; w0 < nrcv; w0 += RCVB * nth) {
         int off[RCVB], dst[RCVB];
-        unsigned wrapm = 0;
+        unsigned wrapm = 0, sysm = 0;
 #pragma unroll
         for (int u = 0; u < RCVB; ++u) {
           dst[u] = -1;
@@ -521,13 +592,15 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
           const int q = w / KK, sl = w - (w / KK) * KK;
           if (q < nfc) {
             const int4 e = rcvtab[q];
-            const int kps = (((1 - nrd) ^ e.z) + e.w + 1) & 1;
+            const int kps = (((1 - nrd) ^ (e.z & 1)) + e.w + 1) & 1;
             const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
             if (e.y >= 0 && valid) {
               off[u] = e.y + sl;
               dst[u] = e.x + sl;
-              if (e.z) wrapm |= 1u << u;
-              v[u] = ld_ll((e.z ? XB2 : XB1) + off[u]);
+              if (e.z & 1) wrapm |= 1u << u;
+              if (e.z & 2) sysm |= 1u << u;
+              const unsigned long long* src = ((e.z & 1) ? XB2 : XB1) + off[u];
+              v[u] = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
             }
           }
         }
@@ -542,7 +615,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
               atomicOr(a.err, 1u);
               timed_out = true;
             }
-            v[u] = ld_ll((w2 ? XB2 : XB1) + off[u]);
+            const unsigned long long* src = (w2 ? XB2 : XB1) + off[u];
+            v[u] = (SLAB && ((sysm >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
           }
           Sd[dst[u]] = __uint_as_float((unsigned)v[u]);
         }
@@ -553,7 +627,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)(n + 2);
     double acc = 0.0;
-    if (!(a.debug & 2)) acc = update_flat<PRESS>(a, S, coltab, pubcol, X, tag, 0, nbnd, KT, nrd, KK, CW, sI, km);
+    unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
+    unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
+    if (!(a.debug & 2))
+      acc = update_flat<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!(a.debug & 2)) acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 5] = gtimer();
@@ -571,11 +648,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
     const int cb = colbase(li, lj);
     // targets: the column itself, plus the halo columns whose closed-form
     // source is this column (les.py:341-355: k first, then j, then i)
-    int ti_[2] = {i, (PRESS && i == 1) ? 0 : -1};
+    int ti_[2] = {i, (PRESS && i == 1 && g.west_bc) ? 0 : -1};  // (a slab's inner x halo is the neighbour's)
     int tj_[3] = {j, (PRESS && j == 1) ? g.jm + 1 : -1, (PRESS && j == g.jm) ? 0 : -1};
     for (int k = lane; k <= km + 1; k += 32) {
       const int kr = k == 0 ? 1 : (k > km ? km : k);
-      const float v = S[cb + colour(i, j, kr) * KK + (kr >> 1)];
+      const float v = S[cb + colour(i + g.ioff, j, kr) * KK + (kr >> 1)];
       const bool own = k >= 1 && k <= km;
       if (own && !finite32(v)) bad = F_PRESS;
       const float hv = (k == km + 1) ? 0.0f : v;
@@ -590,7 +667,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
           a.p[cidx(g, ti_[x], tj_[y], k)] = self && own ? v : hv;
         }
       }
-      if (PRESS && i == g.im) {  // east face is Dirichlet 0 for every j' mapped here
+      if (PRESS && i == g.im && g.east_bc) {  // east face is Dirichlet 0 for every j' mapped here
 #pragma unroll
         for (int y = 0; y < 3; ++y)
           if (tj_[y] >= 0) a.p[cidx(g, g.im + 1, tj_[y], k)] = 0.0f;
@@ -601,7 +678,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(ResArgs a) {
 
   // ---- residuals: tile b sums iteration b over tiles and warps in a fixed order ----
   cg::this_grid().sync();
-  if (tid == 0 && tile == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);  // fresh tags for the next launch
+  // fresh tags for the next launch (a group's slabs share one epoch word)
+  if (tid == 0 && blockIdx.x == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);
   const int per_pass = ntiles * RES_WARPS;
   for (int it = tile; it < a.n_iter; it += ntiles) {
     double tot = 0.0;
@@ -632,20 +710,21 @@ static size_t plan_smem(int tim, int tjm, int kk) {
   return arrays + coltab + pubcol + rcvtab;
 }
 
-ResPlan plan_resident(const Geo& g, int device) {
+ResPlan plan_resident(const Geo& g, int device, int max_tiles) {
   ResPlan pl{};
   pl.ok = false;
   if (g_num_sms < 0) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&g_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   }
-  if (g_num_sms <= 0 || !g.west_bc || !g.east_bc || g.ioff != 0) return pl;
+  if (g_num_sms <= 0) return pl;
+  if (max_tiles <= 0 || max_tiles > g_num_sms) max_tiles = g_num_sms;
   pl.kk = ((g.km + 1) >> 1) + 1;
   pl.kt = (g.km + 1) >> 1;
   size_t best = (size_t)-1;
   // tiles of at least 2 x 2 columns: a column then lies on at most two faces
-  for (int ni = 1; 2 * ni <= g.im && ni <= g_num_sms; ++ni) {
-    for (int nj = 1; 2 * nj <= g.jm && ni * nj <= g_num_sms; ++nj) {
+  for (int ni = 1; 2 * ni <= g.im && ni <= max_tiles; ++ni) {
+    for (int nj = 1; 2 * nj <= g.jm && ni * nj <= max_tiles; ++nj) {
       const int tim = (g.im + ni - 1) / ni, tjm = (g.jm + nj - 1) / nj;
       const size_t smem = plan_smem(tim, tjm, pl.kk);
       if (smem > (size_t)g_max_smem - 2048) continue;
@@ -663,67 +742,99 @@ ResPlan plan_resident(const Geo& g, int device) {
   }
   if (best == (size_t)-1) return pl;
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
-  pl.xbuf = 4LL * pl.ni * pl.nj * 4 * fmax * pl.kk;
+  pl.fstride = (long long)fmax * pl.kk;
+  pl.bstride = (4LL * pl.ni * pl.nj + 2LL * pl.nj) * pl.fstride;  // tile faces + ghost slots
+  pl.xbuf = 4 * pl.bstride;
   pl.ok = true;
   return pl;
 }
 
-bool resident_supported(const Geo& g, const SorC& cf, int device) {
+bool resident_supported(const Geo& g, const SorC& cf, int device, int max_tiles) {
   if (cf.cn1 != nullptr || !cf.uni) return false;  // scalar cn1 and neighbour weights
-  return plan_resident(g, device).ok;
+  return plan_resident(g, device, max_tiles).ok;
 }
 
-int resident_ntiles(const Geo& g, int device) {
-  ResPlan pl = plan_resident(g, device);
+int resident_ntiles(const Geo& g, int device, int max_tiles) {
+  ResPlan pl = plan_resident(g, device, max_tiles);
   return pl.ok ? pl.ni * pl.nj : 0;
 }
 
-int resident_partials(const Geo& g, int device) {
-  ResPlan pl = plan_resident(g, device);
+int resident_partials(const Geo& g, int device, int max_tiles) {
+  ResPlan pl = plan_resident(g, device, max_tiles);
   return pl.ok ? pl.ni * pl.nj * RES_WARPS : 0;
 }
 
-long long resident_xbuf_words(const Geo& g, int device) {
-  ResPlan pl = plan_resident(g, device);
+long long resident_xbuf_words(const Geo& g, int device, int max_tiles) {
+  ResPlan pl = plan_resident(g, device, max_tiles);
   return pl.ok ? pl.xbuf : 0;
 }
 
 static unsigned long long* g_tbuf = nullptr;  // LESB_RES_TRACE stamps of the last launch
 static size_t g_tcap = 0, g_tlen = 0;
 
-template <bool PRESS>
+template <bool PRESS, bool SLAB>
 static cudaError_t set_smem_attr(size_t smem) {
   static size_t attr_set = 0;
   if (attr_set >= smem) return cudaSuccess;
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, k_sor_resident<PRESS>);
+  cudaError_t e = cudaFuncGetAttributes(&fa, k_sor_resident<PRESS, SLAB>);
   if (e != cudaSuccess) return e;
   const int dyn_max = g_max_smem - (int)fa.sharedSizeBytes;
-  e = cudaFuncSetAttribute(k_sor_resident<PRESS>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+  e = cudaFuncSetAttribute(k_sor_resident<PRESS, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
   if (e != cudaSuccess) return e;
   attr_set = (size_t)dyn_max;
   return cudaSuccess;
 }
 
-// One launch does the whole solve: n_iter iterations, the press halo (policy
-// 1) with its non-finite check into pflags, and res[n_iter].  xbuf holds
-// resident_xbuf_words() 64-bit words, zeroed once; *epoch starts at 0 and is
-// advanced by every launch (both are reset after a timeout).
-cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float* rhs, const SorC& cf, float om,
-                                int n_iter, int policy, void* xbuf, unsigned* epoch, double* partials,
-                                double* res, unsigned* pflags, unsigned* err, cudaStream_t st) {
-  ResPlan pl = plan_resident(g, device);
-  if (!pl.ok || !cf.uni || cf.cn1) return cudaErrorInvalidValue;
-  cudaError_t e = policy == 1 ? set_smem_attr<true>(pl.smem) : set_smem_attr<false>(pl.smem);
+static cudaError_t launch_group(ResGroup& grp, int policy, bool slab, size_t smem, cudaStream_t st) {
+  cudaError_t e = policy == 1 ? (slab ? set_smem_attr<true, true>(smem) : set_smem_attr<true, false>(smem))
+                              : (slab ? set_smem_attr<false, true>(smem) : set_smem_attr<false, false>(smem));
   if (e != cudaSuccess) return e;
-  const int ntiles = pl.ni * pl.nj;
-  ResArgs a{g,      pl,     p,      rhs,  om,    cf.cn1s,  cf.w2l, cf.w2s, cf.w3l, cf.w3s,
-            cf.w4l, cf.w4s, n_iter, (unsigned long long*)xbuf, epoch, partials, res, pflags, err, 0};
+  void* args[] = {&grp};
+  const void* fn = policy == 1 ? (slab ? (const void*)k_sor_resident<true, true> : (const void*)k_sor_resident<true, false>)
+                               : (slab ? (const void*)k_sor_resident<false, true> : (const void*)k_sor_resident<false, false>);
+  return cudaLaunchCooperativeKernel(fn, dim3(grp.n * grp.tps), dim3(RES_THREADS), args, smem, st);
+}
+
+static ResArgs make_args(const ResidentCall& c, const ResPlan& pl) {
+  ResArgs a{};
+  a.g = *c.g;
+  a.pl = pl;
+  a.p = c.p;
+  a.rhs = c.rhs;
+  a.om = c.om;
+  a.cn1 = c.cf->cn1s;
+  a.w2l = c.cf->w2l; a.w2s = c.cf->w2s; a.w3l = c.cf->w3l; a.w3s = c.cf->w3s; a.w4l = c.cf->w4l; a.w4s = c.cf->w4s;
+  a.n_iter = c.n_iter;
+  a.xbuf = (unsigned long long*)c.xbuf;
+  a.epoch = c.epoch;
+  a.partials = c.partials;
+  a.res = c.res;
+  a.pflags = c.pflags;
+  a.err = c.err;
+  a.peer_w = (unsigned long long*)c.peer_w;
+  a.peer_e = (unsigned long long*)c.peer_e;
   static const int dbg = getenv("LESB_RES_DEBUG") ? atoi(getenv("LESB_RES_DEBUG")) : 0;
   a.debug = dbg;
   a.trace = nullptr;
+  return a;
+}
+
+// One launch does the whole solve: n_iter iterations, the press halo (policy
+// 1) with its non-finite check into pflags, and res[n_iter].  xbuf holds
+// resident_xbuf_words() 64-bit words, zeroed once; *epoch starts at 0 and is
+// advanced by every launch (both are reset after a timeout).  With peer_w /
+// peer_e set the domain is an x-slab whose neighbours run the same plan on
+// other GPUs (their face buffers mapped here), launched at the same time.
+cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st) {
+  ResPlan pl = plan_resident(*c.g, c.device, 0);
+  if (!pl.ok || !c.cf->uni || c.cf->cn1) return cudaErrorInvalidValue;
+  ResGroup grp{};
+  grp.a[0] = make_args(c, pl);
+  grp.n = 1;
+  grp.tps = pl.ni * pl.nj;
   static const bool trace = getenv("LESB_RES_TRACE") != nullptr;
-  const size_t tneed = (size_t)ntiles * 2 * n_iter * NST;
+  const size_t tneed = (size_t)grp.tps * 2 * c.n_iter * NST;
   if (trace) {
     if (g_tcap < tneed) {
       if (g_tbuf) cudaFree(g_tbuf);
@@ -731,11 +842,39 @@ cudaError_t launch_sor_resident(const Geo& g, int device, float* p, const float*
       g_tcap = tneed;
     }
     g_tlen = tneed;
-    a.trace = g_tbuf;
+    grp.a[0].trace = g_tbuf;
   }
-  void* args[] = {&a};
-  const void* fn = policy == 1 ? (const void*)k_sor_resident<true> : (const void*)k_sor_resident<false>;
-  return cudaLaunchCooperativeKernel(fn, dim3(ntiles), dim3(RES_THREADS), args, pl.smem, st);
+  return launch_group(grp, c.policy, c.peer_w || c.peer_e, pl.smem, st);
+}
+
+// n in-process x-slabs of one device (west to east), one cooperative launch:
+// each slab gets num_SMs / n tiles; the slabs' x faces move through each
+// other's ghost slots like the cross-GPU case.  All slabs must share
+// (im, jm, km) (so they share the plan) and one epoch word.
+cudaError_t launch_sor_resident_group(int n, const ResidentCall* cs, cudaStream_t st) {
+  if (n < 1 || n > RES_GROUP_MAX) return cudaErrorInvalidValue;
+  ResPlan pl = plan_resident(*cs[0].g, cs[0].device, resident_group_tiles(n));
+  if (!pl.ok) return cudaErrorInvalidValue;
+  ResGroup grp{};
+  for (int s = 0; s < n; ++s) {
+    if (!cs[s].cf->uni || cs[s].cf->cn1) return cudaErrorInvalidValue;
+    grp.a[s] = make_args(cs[s], pl);
+  }
+  grp.n = n;
+  grp.tps = pl.ni * pl.nj;
+  return launch_group(grp, cs[0].policy, true, pl.smem, st);
+}
+
+int resident_group_max() { return RES_GROUP_MAX; }
+
+int resident_group_tiles(int n) {
+  if (g_num_sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&g_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return g_num_sms > 0 && n > 0 ? (g_num_sms / n > 0 ? g_num_sms / n : 1) : 1;
 }
 
 }  // namespace lesb

@@ -30,17 +30,28 @@ def single(P, st, inflow, n_steps, n_iter, scheme):
     return out
 
 
+@pytest.mark.parametrize("solver", ["resident", "passes"])
 @pytest.mark.parametrize("dims,nslabs,scheme", [
     ((24, 10, 8), 2, "redblack"),
     ((24, 10, 8), 3, "redblack"),
-    ((9, 7, 5), 3, "redblack"),      # odd jm, uneven slabs
+    ((9, 7, 5), 3, "redblack"),      # odd jm, equal slabs of 3 planes
+    ((10, 7, 5), 3, "redblack"),     # uneven slabs: streaming passes
     ((16, 12, 10), 4, "twinned"),
     ((32, 32, 16), 4, "redblack"),
+    ((48, 40, 20), 2, "redblack"),   # several resident tiles per slab in x and y
 ])
-def test_slabs_equal_single_domain(dims, nslabs, scheme):
+def test_slabs_equal_single_domain(dims, nslabs, scheme, solver, monkeypatch):
+    """Red-black slabs of one shape run the resident solver as one group
+    launch (tile faces cross slab boundaries through ghost slots, the
+    in-process form of the NVLink peer path); LESB_GROUP_PASSES forces the
+    streaming colour passes with plane copies."""
     import paper_1504_02264_b200 as P
     from paper_1504_02264_b200.slabs import SlabGroup
 
+    if solver == "passes":
+        monkeypatch.setenv("LESB_GROUP_PASSES", "1")
+    else:
+        monkeypatch.delenv("LESB_GROUP_PASSES", raising=False)
     P.runtime.set_sor_path(0)
     st = gi.random_state(*dims, seed=sum(dims) * 7 + nslabs, vel_scale=0.3)
     inflow = gi.random_inflow(dims[2], seed=5)
