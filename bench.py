@@ -185,7 +185,7 @@ def cpu_sample(max_steps: int, budget_s: float):
     import golden_inputs as gi
     from oracle import les_oracle as O
 
-    st = gi.config2_state()
+    st = gi.config2_state(IM, JM, KM)
     o = O.OState.zeros(IM, JM, KM)
     for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask", "dx1", "dy1", "dzn"):
         getattr(o, n)[...] = st[n]
@@ -209,7 +209,7 @@ def run_reference(args):
         cpu_sample(1, 0)
     rate, n, secs = cpu_sample(max(1, args.steps), 90.0)
     cores = 1
-    sample = f"{n} full 150x150x90 RB50 steps of the numpy port (oracle/les_oracle.py), 1 thread"
+    sample = f"{n} full {IM}x{JM}x{KM} RB50 steps of the numpy port (oracle/les_oracle.py), 1 thread"
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1000.0 / rate, "higher_is_better": True,
@@ -242,7 +242,7 @@ def run_gpu(args):
 
     P.runtime.set_device(local)
     lib = N.load()
-    st0 = gi.config2_state()
+    st0 = gi.config2_state(IM, JM, KM)
     inflow = P.WindProfile(*gi.default_inflow(KM))
     slab_dom = None
     if world == 1:
@@ -478,6 +478,7 @@ def e2e_slabs(dom, gstate, inflow, torch, args, world):
 
 
 def main():
+    global IM, JM, KM, WORKLOAD
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)
@@ -485,7 +486,13 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e measurement (profiling runs)")
+    ap.add_argument("--grid", type=int, nargs=3, metavar=("IM", "JM", "KM"),
+                    help="another grid (per GPU) with config 2's buildings scaled to it; default config 2")
     args = ap.parse_args()
+    if args.grid and tuple(args.grid) != (IM, JM, KM):
+        IM, JM, KM = args.grid
+        WORKLOAD = (f"config2 layout scaled to {IM}x{JM}x{KM}, h=2, dt=0.5, 3x3 buildings, log-law inflow, "
+                    f"RB SOR 50 iters")
     if args.warmup < 3 and args.impl == "cuda":
         args.warmup = 3
     if args.impl == "reference":

@@ -242,9 +242,10 @@ bool map_slab_peers(lesb_domain* h) {
 }
 
 int ensure_partials(lesb_domain* h, int n_iter) {
-  long long need = (long long)n_iter * 2 *
-                   std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)), resident_partials(h->g, h->device)),
-                            std::max(sor_blocks_fused(h->g, h->device), sor_blocks_march(h->g, h->device)));
+  const int maxblk = std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)),
+                                        resident_partials(h->g, h->device)),
+                               std::max(sor_blocks_fused(h->g, h->device), sor_blocks_march(h->g, h->device)));
+  long long need = (long long)n_iter * 2 * maxblk + reduce_scratch(maxblk, n_iter);
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
     h->partials = nullptr;

@@ -65,10 +65,13 @@ __device__ __forceinline__ long long cidx(const Geo& g, int i, int j, int k) {
 
 // OR the per-thread stage bits into the flag word: one atomic per warp at most.
 // All 32 lanes of every warp must call this (kernels never return early).
+// One atomic per warp that has a bit to add -- and none once the word holds
+// them all: a field that went non-finite everywhere must not turn every warp
+// of a whole-array kernel into an atomic on one address.
 __device__ __forceinline__ void flag_or(unsigned* flags, unsigned bits) {
   unsigned any = __reduce_or_sync(0xffffffffu, bits);
   unsigned tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  if (any && (tid & 31u) == 0) atomicOr(flags, any);
+  if (any && (tid & 31u) == 0 && (*(volatile unsigned*)flags & any) != any) atomicOr(flags, any);
 }
 
 // Deterministic block reduction of a double (fixed shuffle tree, fixed warp order).

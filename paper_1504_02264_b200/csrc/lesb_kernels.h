@@ -67,6 +67,7 @@ void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rh
 void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st);
 void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned* flags, cudaStream_t st);
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st);
+int reduce_scratch(int nblk, int n_iter);  // extra doubles launch_reduce_res needs after the partials
 int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused);
 cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
                         int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,

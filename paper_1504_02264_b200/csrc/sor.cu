@@ -193,6 +193,60 @@ __global__ void k_press_halo(Geo g, const float* src, float* dst, unsigned* flag
   if (flags) flag_or(flags, bits);
 }
 
+// The same by rows: a warp takes PH_R consecutive (i, j) rows, lanes over k
+// (one row decode per warp instead of a div/mod per element, all PH_R rows'
+// loads in flight at once).  The 3-D launch above is latency bound (one
+// dependent load per thread: ~470 us on 600x600x90, ~300 GB/s); this is
+// bound by HBM.
+constexpr int PH_R = 4, PH_WARPS = 8;
+template <int NK>
+__global__ void __launch_bounds__(PH_WARPS * 32) k_press_halo_rows(Geo g, const float* src, float* dst,
+                                                                    unsigned* flags) {
+  const int lane = threadIdx.x & 31;
+  const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  const long long r0 = ((long long)blockIdx.x * PH_WARPS + (threadIdx.x >> 5)) * PH_R;
+  float val[PH_R][NK];
+  unsigned bits = 0;
+#pragma unroll
+  for (int q = 0; q < PH_R; ++q) {
+    const long long row = r0 + q;
+    const int i = (int)(row / (g.jm + 2)), j = (int)(row - (long long)i * (g.jm + 2));
+    const bool rowhalo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1;
+    const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+    // the row whose values this row takes: itself, or (press) its closed-form source
+    const bool zero_row = rowhalo && !foreign && i == g.im + 1;
+    const int ii = (rowhalo && !foreign && i == 0) ? 1 : i;
+    const int jj = (rowhalo && !foreign) ? (j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j)) : j;
+    const float* s = src + cidx(g, ii, jj, 0);
+#pragma unroll
+    for (int u = 0; u < NK; ++u) {
+      const int k = lane + 32 * u;
+      val[q][u] = 0.0f;
+      if (row >= nrow || k > g.km + 1 || zero_row) continue;
+      const int kk = (foreign || k > 0) ? k : 1;   // bottom: p[.,.,0] -> p[.,.,1]
+      val[q][u] = (!foreign && k == g.km + 1) ? 0.0f : s[kk];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PH_R; ++q) {
+    const long long row = r0 + q;
+    if (row >= nrow) continue;
+    const int i = (int)(row / (g.jm + 2)), j = (int)(row - (long long)i * (g.jm + 2));
+    const bool rowhalo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1;
+    const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+    float* d = dst + cidx(g, i, j, 0);
+#pragma unroll
+    for (int u = 0; u < NK; ++u) {
+      const int k = lane + 32 * u;
+      if (k > g.km + 1) continue;
+      const bool halo = !foreign && (rowhalo || k == 0 || k == g.km + 1);
+      if (halo || src != dst) d[k] = val[q][u];
+      if (flags && !finite32(val[q][u])) bits = F_PRESS;
+    }
+  }
+  if (flags) flag_or(flags, bits);
+}
+
 // residuals[it] = (sum of pass-0 partials) + (sum of pass-1 partials), each
 // summed by one fixed-order tree (deterministic; numpy's pairwise order is
 // matched only to rtol ~1e-15).
@@ -259,16 +313,59 @@ void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st)
 }
 
 void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned* flags, cudaStream_t st) {
-  int nk = g.km + 2;
-  int bx = ((nk + 31) / 32) * 32;
+  const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  const unsigned nblk = (unsigned)((nrow + PH_R * PH_WARPS - 1) / (PH_R * PH_WARPS));
+  const int nk = (g.km + 2 + 31) / 32;
+  static const int mode = getenv("LESB_PH_MODE") ? atoi(getenv("LESB_PH_MODE")) : 1;
+  if (mode == 1 && nk <= 4) {
+    switch (nk) {
+      case 1: k_press_halo_rows<1><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;
+      case 2: k_press_halo_rows<2><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;
+      case 3: k_press_halo_rows<3><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;
+      default: k_press_halo_rows<4><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;
+    }
+  }
+  int bx = ((g.km + 2 + 31) / 32) * 32;
   if (bx > 128) bx = 128;
   int by = 256 / bx;
-  dim3 grid((nk + bx - 1) / bx, (g.jm + 2 + by - 1) / by, g.im + 2);
+  dim3 grid((g.km + 2 + bx - 1) / bx, (g.jm + 2 + by - 1) / by, g.im + 2);
   k_press_halo<<<grid, dim3(bx, by), 0, st>>>(g, src, dst, flags);
 }
 
+// Stage 1 of the residual reduction for long partial rows: block (c, r) sums
+// chunk c (RED_CHUNK consecutive partials) of row r = 2 it + pass, in a fixed
+// order, so the two-stage sum is deterministic.
+constexpr int RED_CHUNK = 4096;
+__global__ void k_reduce_chunks(const double* __restrict__ partials, int nblk, int nch, double* __restrict__ out) {
+  __shared__ double red[8];
+  const int c = blockIdx.x, r = blockIdx.y;
+  const double* q = partials + (long long)r * nblk + (long long)c * RED_CHUNK;
+  const int n = min(RED_CHUNK, nblk - c * RED_CHUNK);
+  double a = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) a += q[b];
+  a = block_sum<8>(a, red);
+  if (threadIdx.x == 0) out[(long long)r * nch + c] = a;
+}
+
+int reduce_scratch(int nblk, int n_iter) {
+  const int nch = (nblk + RED_CHUNK - 1) / RED_CHUNK;
+  return nch > 1 ? 2 * n_iter * nch : 0;
+}
+
+// res[it] = sum over both passes of iteration it of the per-block partials
+// ([n_iter][2][nblk]).  Rows longer than one chunk are first cut into chunk
+// sums (written after the partials: the caller sizes the buffer with
+// reduce_scratch), so a 600x600x90 solve reduces in microseconds instead of
+// one 256-thread block per iteration walking ~150k partials.
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st) {
-  k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
+  const int nch = (nblk + RED_CHUNK - 1) / RED_CHUNK;
+  if (nch <= 1) {
+    k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
+    return;
+  }
+  double* scratch = const_cast<double*>(partials) + (long long)2 * n_iter * nblk;
+  k_reduce_chunks<<<dim3(nch, 2 * n_iter), 256, 0, st>>>(partials, nblk, nch, scratch);
+  k_reduce_res<<<n_iter, 256, 0, st>>>(scratch, nch, out);
 }
 
 int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused) {

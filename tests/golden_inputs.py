@@ -122,11 +122,13 @@ def config1_state():
     return st
 
 
-def config2_state():
-    st = zero_state(150, 150, 90)
+def config2_state(im=150, jm=150, km=90):
+    """Config 2 (150x150x90, 3x3 buildings); other sizes scale the building
+    layout to the grid (bench.py --grid)."""
+    st = zero_state(im, jm, km)
     for bi in range(3):
         for bj in range(3):
-            i0, j0 = 30 + 40 * bi, 30 + 40 * bj
-            h = 10 + 10 * ((bi + bj) % 3)
-            st["mask"][i0:i0 + 16, j0:j0 + 16, 1:1 + h] = 1.0
+            i0, j0 = (30 + 40 * bi) * im // 150, (30 + 40 * bj) * jm // 150
+            h = (10 + 10 * ((bi + bj) % 3)) * km // 90
+            st["mask"][i0:i0 + 16 * im // 150, j0:j0 + 16 * jm // 150, 1:1 + h] = 1.0
     return st
