@@ -28,6 +28,7 @@ namespace lesb {
 
 constexpr int RB_NT = 256;  // threads per colour-pass block: x = colour cells of a column, y = j
 constexpr int RB_NW = RB_NT / 32;
+constexpr int RB_R = 4;     // rows per thread (j, j + by, ...)
 
 // Block shape of a colour pass: x spans the colour's cells of a column (so a
 // warp runs on into the next j row instead of idling), y the rows.
@@ -92,25 +93,40 @@ __global__ void __launch_bounds__(RB_NT) k_sor_rb(Geo g, float* __restrict__ p, 
                                                          double* __restrict__ partials) {
   __shared__ double red[RB_NW];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y + 1;
   const int i = blockIdx.z + 1;
-  double acc = 0.0;
-  if (j <= g.jm) {
-    const int ig0 = i + g.ioff - 1;
+  const int ig0 = i + g.ioff - 1;
+  // RB_R rows per thread (j0, j0 + by, ...): every row's loads are issued
+  // before the first store -- a colour pass writes only its own colour and
+  // reads only the other one plus the centre, so nothing aliases -- which
+  // keeps RB_R times more bytes in flight per thread
+  float pc[RB_R], rel[RB_R];
+  long long cc[RB_R];
+  bool ok[RB_R];
+#pragma unroll
+  for (int q = 0; q < RB_R; ++q) {
+    const int j = (blockIdx.y * RB_R + q) * blockDim.y + threadIdx.y + 1;
     const int k = 1 + ((ig0 + (j - 1) + nrd) & 1) + 2 * t;
-    if (k <= g.km) {
-      float pc, rel;
-      if (UNI) {
-        const int c = i * (int)g.si + j * g.sj + k;
-        rel = sor_point<POL, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
-        p[c] = pc + rel;
-      } else {
-        const long long c = cidx(g, i, j, k);
-        rel = sor_point<POL>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc);
-        p[c] = pc + rel;
-      }
-      acc = (double)rel * (double)rel;
+    ok[q] = j <= g.jm && k <= g.km;
+    cc[q] = 0;
+    rel[q] = 0.0f;
+    pc[q] = 0.0f;
+    if (!ok[q]) continue;
+    if (UNI) {
+      const int c = i * (int)g.si + j * g.sj + k;
+      cc[q] = c;
+      rel[q] = sor_point<POL, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc[q]);
+    } else {
+      const long long c = cidx(g, i, j, k);
+      cc[q] = c;
+      rel[q] = sor_point<POL>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc[q]);
     }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < RB_R; ++q) {
+    if (!ok[q]) continue;
+    p[cc[q]] = pc[q] + rel[q];
+    acc += (double)rel[q] * (double)rel[q];
   }
   // fixed-order block reduction over the block's (possibly partial) warps
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -272,7 +288,7 @@ int sor_blocks_rb(const Geo& g) {
   const int kh = (g.km + 1) / 2;
   int bx, by;
   rb_shape(g, &bx, &by);
-  return ((kh + bx - 1) / bx) * ((g.jm + by - 1) / by) * g.im;
+  return ((kh + bx - 1) / bx) * ((g.jm + by * RB_R - 1) / (by * RB_R)) * g.im;
 }
 int sor_blocks_tw(const Geo& g) {
   return ((g.km + TW_BX - 1) / TW_BX) * ((g.jm + TW_BY - 1) / TW_BY) * g.im;
@@ -283,7 +299,7 @@ void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, fl
   const int kh = (g.km + 1) / 2;
   int bx, by;
   rb_shape(g, &bx, &by);
-  dim3 grid((kh + bx - 1) / bx, (g.jm + by - 1) / by, g.im);
+  dim3 grid((kh + bx - 1) / bx, (g.jm + by * RB_R - 1) / (by * RB_R), g.im);
   dim3 block(bx, by);
   const int y_stored = (policy == 1 && (g.jm & 1)) ? 1 : 0;
   if (y_stored) {
