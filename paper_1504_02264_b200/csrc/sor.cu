@@ -332,8 +332,7 @@ void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
   const unsigned nblk = (unsigned)((nrow + PH_R * PH_WARPS - 1) / (PH_R * PH_WARPS));
   const int nk = (g.km + 2 + 31) / 32;
-  static const int mode = getenv("LESB_PH_MODE") ? atoi(getenv("LESB_PH_MODE")) : 1;
-  if (mode == 1 && nk <= 4) {
+  if (nk <= 4) {  // km + 2 <= 128: rows (otherwise the 3-D launch)
     switch (nk) {
       case 1: k_press_halo_rows<1><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;
       case 2: k_press_halo_rows<2><<<nblk, PH_WARPS * 32, 0, st>>>(g, src, dst, flags); return;

@@ -176,11 +176,14 @@ def test_quiescent_fixed_point(P):
 
 def test_step_against_oracle_odd_shapes(P):
     """Extra shapes the golden set does not cover (odd jm with RB, jm = 1,
-    km = 1), GPU vs the CPU oracle for 4 steps."""
+    km = 1, deep columns), GPU vs the CPU oracle for 4 steps."""
     from oracle import les_oracle as O
 
+    # (deep columns: the row-wise press halo for km + 2 <= 128 in 1..4 warps'
+    # width, the 3-D launch above that)
     for (im, jm, km), scheme in (((7, 5, 3), "redblack"), ((5, 1, 4), "redblack"), ((6, 4, 1), "twinned"),
-                                 ((3, 3, 3), "twinned")):
+                                 ((3, 3, 3), "twinned"), ((5, 4, 30), "redblack"), ((4, 5, 94), "redblack"),
+                                 ((4, 3, 126), "redblack"), ((4, 3, 131), "redblack")):
         st = gi.random_state(im, jm, km, seed=im * 100 + jm * 10 + km, vel_scale=0.2)
         inflow = gi.random_inflow(km, seed=7)
         fs = dstate(P, st)
