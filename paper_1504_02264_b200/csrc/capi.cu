@@ -1227,7 +1227,32 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
                               h->partials,  h->res_d,   &h->book_d->flags,     &h0->book_d->err,
                               s > 0 ? hs[s - 1]->gxbuf : nullptr, s < n - 1 ? hs[s + 1]->gxbuf : nullptr};
     }
-    CK(launch_sor_resident_group(n, calls.data(), st));
+    if (!std::getenv("LESB_GROUP_SEPARATE")) {
+      CK(launch_sor_resident_group(n, calls.data(), st));
+    } else {
+      // Test form of the multi-GPU path: every slab its own cooperative launch
+      // on its own stream with its own epoch, exchanging through the
+      // neighbours' ghost slots -- as NCCL ranks do across GPUs (each launch
+      // keeps num_SMs / n tiles so the n launches can be co-resident).
+      cudaEvent_t ev_in;
+      CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev_in, st));
+      std::vector<cudaEvent_t> ev_out(n);
+      for (int s = 0; s < n; ++s) {
+        lesb_domain* h = hs[s];
+        calls[s].epoch = h->gepoch;
+        calls[s].max_tiles = resident_group_tiles(n);
+        CK(cudaStreamWaitEvent(h->st, ev_in, 0));
+        CK(launch_sor_resident(calls[s], h->st));
+        CK(cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_out[s], h->st));
+      }
+      for (int s = 0; s < n; ++s) {
+        CK(cudaStreamWaitEvent(st, ev_out[s], 0));
+        cudaEventDestroy(ev_out[s]);
+      }
+      cudaEventDestroy(ev_in);
+    }
   }
   for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {

@@ -108,6 +108,7 @@ struct ResidentCall {
   unsigned* err;
   void* peer_w;  // x-slab neighbours' face buffers (another GPU's, mapped), or nullptr
   void* peer_e;
+  int max_tiles = 0;  // tiles of the plan (0: every SM); slabs sharing a device use num_SMs / n
 };
 cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st);
 cudaError_t launch_sor_resident_group(int n, const ResidentCall* cs, cudaStream_t st);

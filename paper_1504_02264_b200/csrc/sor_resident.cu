@@ -827,7 +827,7 @@ static ResArgs make_args(const ResidentCall& c, const ResPlan& pl) {
 // peer_e set the domain is an x-slab whose neighbours run the same plan on
 // other GPUs (their face buffers mapped here), launched at the same time.
 cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st) {
-  ResPlan pl = plan_resident(*c.g, c.device, 0);
+  ResPlan pl = plan_resident(*c.g, c.device, c.max_tiles);
   if (!pl.ok || !c.cf->uni || c.cf->cn1) return cudaErrorInvalidValue;
   ResGroup grp{};
   grp.a[0] = make_args(c, pl);

@@ -30,7 +30,7 @@ def single(P, st, inflow, n_steps, n_iter, scheme):
     return out
 
 
-@pytest.mark.parametrize("solver", ["resident", "passes"])
+@pytest.mark.parametrize("solver", ["resident", "separate", "passes"])
 @pytest.mark.parametrize("dims,nslabs,scheme", [
     ((24, 10, 8), 2, "redblack"),
     ((24, 10, 8), 3, "redblack"),
@@ -43,15 +43,19 @@ def single(P, st, inflow, n_steps, n_iter, scheme):
 def test_slabs_equal_single_domain(dims, nslabs, scheme, solver, monkeypatch):
     """Red-black slabs of one shape run the resident solver as one group
     launch (tile faces cross slab boundaries through ghost slots, the
-    in-process form of the NVLink peer path); LESB_GROUP_PASSES forces the
-    streaming colour passes with plane copies."""
+    in-process form of the NVLink peer path); LESB_GROUP_SEPARATE launches
+    every slab on its own stream with its own epoch (what each rank does on
+    its own GPU); LESB_GROUP_PASSES forces the streaming colour passes with
+    plane copies."""
     import paper_1504_02264_b200 as P
     from paper_1504_02264_b200.slabs import SlabGroup
 
+    monkeypatch.delenv("LESB_GROUP_PASSES", raising=False)
+    monkeypatch.delenv("LESB_GROUP_SEPARATE", raising=False)
     if solver == "passes":
         monkeypatch.setenv("LESB_GROUP_PASSES", "1")
-    else:
-        monkeypatch.delenv("LESB_GROUP_PASSES", raising=False)
+    elif solver == "separate":  # one launch per slab, own stream and epoch: the per-GPU form
+        monkeypatch.setenv("LESB_GROUP_SEPARATE", "1")
     P.runtime.set_sor_path(0)
     st = gi.random_state(*dims, seed=sum(dims) * 7 + nslabs, vel_scale=0.3)
     inflow = gi.random_inflow(dims[2], seed=5)
