@@ -52,7 +52,7 @@ namespace lesb {
 constexpr int RES_THREADS = 512;
 constexpr int RES_WARPS = RES_THREADS / 32;
 constexpr int NST = 6;   // LESB_RES_TRACE stamps per pass
-constexpr int RCVB = 6;  // face values each thread has in flight while receiving
+constexpr int RCVP = 3;  // receive slot pairs each thread keeps in registers  // face values each thread has in flight while receiving
 
 struct ResPlan {
   int ni, nj;       // tile grid
@@ -109,6 +109,14 @@ __device__ __forceinline__ unsigned long long ld_ll_sys(const unsigned long long
   unsigned long long w;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
   return w;
+}
+__device__ __forceinline__ void ld_ll2(const unsigned long long* a, unsigned long long& x, unsigned long long& y) {
+  // two LL words in one 16-byte load (each 8-byte element single-copy atomic)
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a));
+}
+__device__ __forceinline__ void ld_ll2_sys(const unsigned long long* a, unsigned long long& x,
+                                           unsigned long long& y) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a));
 }
 __device__ __forceinline__ unsigned long long ld_ll(const unsigned long long* a) {
   unsigned long long w;
@@ -358,6 +366,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   const int J0 = tile_lo(tj, g.jm, pl.nj), J1 = tile_lo(tj + 1, g.jm, pl.nj);
   const int TI = I1 - I0, TJ = J1 - J0;
   const int KK = pl.kk, KT = pl.kt, km = g.km;
+  const int KKF = (KK + 1) & ~1;  // face-buffer words per column: even, so slot pairs are 16-byte aligned
   const int CW = 4 * KK + 1;                 // floats per column (odd: lanes in different columns spread over banks)
   // column stride along i, padded so that sI = (TJ - 2) CW (mod 32): the
   // interior columns then sit at CW * (ordinal) + const modulo the 32 banks,
@@ -414,11 +423,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
                 ((wtile && li == 1) ? (1u << 29) : 0u);
     // face words of the column: west / east face (x), south / north face (y)
     // (an x face of an edge tile goes to the neighbour slab's ghost slot)
-    const int fx = li == 1 ? ((ti == 0 && pw) ? (PUB_RW | ((lj - 1) * KK)) : (int)(0 * fstride + (lj - 1) * KK))
-                           : (li == TI ? ((ti == pl.ni - 1 && pe) ? (PUB_RE | ((lj - 1) * KK))
-                                                                  : (int)(1 * fstride + (lj - 1) * KK))
+    const int fx = li == 1 ? ((ti == 0 && pw) ? (PUB_RW | ((lj - 1) * KKF)) : (int)(0 * fstride + (lj - 1) * KKF))
+                           : (li == TI ? ((ti == pl.ni - 1 && pe) ? (PUB_RE | ((lj - 1) * KKF))
+                                                                  : (int)(1 * fstride + (lj - 1) * KKF))
                                        : -1);
-    const int fy = lj == 1 ? (int)(2 * fstride + (li - 1) * KK) : (lj == TJ ? (int)(3 * fstride + (li - 1) * KK) : -1);
+    const int fy = lj == 1 ? (int)(2 * fstride + (li - 1) * KKF) : (lj == TJ ? (int)(3 * fstride + (li - 1) * KKF) : -1);
     // (tiles are at least 2 x 2 columns, so no column lies on more faces)
     pubcol[c] = fx >= 0 ? make_int2(fx, fy) : make_int2(fy, -1);
   }
@@ -436,9 +445,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     const int sj_ = sj0 == 0 ? g.jm : (sj0 == g.jm + 1 ? 1 : sj0);
     // (halo column, source word, wrap flip | ghost << 1, source parity)
     const int nf = nbr[f];
-    const long long src_off = nf >= 0 ? nf * tstride + (f ^ 1) * fstride + m * KK
-                              : nf == -2 ? ghost_w + m * KK
-                              : nf == -3 ? ghost_e + m * KK
+    const long long src_off = nf >= 0 ? nf * tstride + (f ^ 1) * fstride + m * KKF
+                              : nf == -2 ? ghost_w + m * KKF
+                              : nf == -3 ? ghost_e + m * KKF
                                          : -1;
     rcvtab[q] = make_int4(colbase(rli, rlj), (int)src_off, (wrap ? wrap_flip : 0) | (nf < -1 ? 2 : 0),
                           (si_ + g.ioff + sj_) & 1);
@@ -511,17 +520,20 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   const int nint = ncol - nbnd;
   const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
   const int L_i = (KT + nseg_i - 1) / nseg_i;
-  // receive walk over (face column q, slot sl): item w = tid + nth u.  The
-  // first RCVB items of every thread keep their descriptors in registers for
-  // the whole solve (source word, halo slot, wrap bit, and per colour whether
-  // the slot holds a published cell); any further items are decoded per pass.
-  const int nrcv = nfc * KK;
-  int roff[RCVB], rdst[RCVB];
+  // receive walk over slot PAIRS (face column q, slots sl, sl + 1; sl even):
+  // pair w = tid + nth u, one 16-byte load each (two LL words).  The first
+  // RCVP pairs of every thread keep their descriptors in registers for the
+  // whole solve (source word, halo slot, wrap / ghost bits, and per colour
+  // which of the two slots hold a published cell); further pairs are decoded
+  // per pass.
+  const int HP = KKF >> 1;  // pairs per face column
+  const int nrcv = nfc * HP;
+  int roff[RCVP], rdst[RCVP];
   unsigned rwrap = 0, rsys = 0, rval0 = 0, rval1 = 0;
 #pragma unroll
-  for (int u = 0; u < RCVB; ++u) {
+  for (int u = 0; u < RCVP; ++u) {
     const int w = tid + nth * u;
-    const int q = w / KK, sl = w - (w / KK) * KK;
+    const int q = w / HP, sl = 2 * (w - (w / HP) * HP);
     roff[u] = 0;
     rdst[u] = -1;
     if (q < nfc) {
@@ -532,12 +544,16 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
         if (e.z & 1) rwrap |= 1u << u;
         if (e.z & 2) rsys |= 1u << u;  // a ghost slot, written by a neighbour slab
         // only slots holding cells of the source colour were published
-        // (bit u of rval<c>: the slot is valid in the passes of colour c)
+        // (bits 2u, 2u+1 of rval<c>: slot sl / sl+1 valid in passes of colour c)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int kps = (((1 - c) ^ (e.z & 1)) + e.w + 1) & 1;
-          const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
-          if (valid) (c ? rval1 : rval0) |= 1u << u;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int s2 = sl + h;
+            const bool valid = kps ? s2 <= ((km - 1) >> 1) : (s2 >= 1 && s2 <= ((km - 2) >> 1) + 1);
+            if (valid) (c ? rval1 : rval0) |= 1u << (2 * u + h);
+          }
         }
       }
     }
@@ -558,67 +574,59 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
       float* Sd = S + (1 - nrd) * KK;
       const unsigned vm = nrd ? rval1 : rval0;
-      unsigned long long v[RCVB];
+      unsigned long long v[RCVP][2];
 #pragma unroll
-      for (int u = 0; u < RCVB; ++u)
-        if ((vm >> u) & 1u) {
+      for (int u = 0; u < RCVP; ++u)
+        if ((vm >> (2 * u)) & 3u) {
           const unsigned long long* src = (((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u];
-          v[u] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
+          if (SLAB && ((rsys >> u) & 1u)) ld_ll2_sys(src, v[u][0], v[u][1]);
+          else ld_ll2(src, v[u][0], v[u][1]);
         }
 #pragma unroll
-      for (int u = 0; u < RCVB; ++u) {
-        if (!((vm >> u) & 1u)) continue;
+      for (int u = 0; u < RCVP; ++u) {
         const bool w2 = (rwrap >> u) & 1u;
         const unsigned want = w2 ? t2 : t1;
-        unsigned spins = 0;
-        while ((unsigned)(v[u] >> 32) != want && !timed_out && !(a.debug & 1)) {
-          if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
-            atomicOr(a.err, 1u);
-            timed_out = true;
-          }
-          const unsigned long long* src = (w2 ? XB2 : XB1) + roff[u];
-          v[u] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
-        }
-        Sd[rdst[u]] = __uint_as_float((unsigned)v[u]);
-      }
-      // items beyond the register-held ones (large tiles / deep columns)
-      for (int w0 = RCVB * nth; w0 < nrcv; w0 += RCVB * nth) {
-        int off[RCVB], dst[RCVB];
-        unsigned wrapm = 0, sysm = 0;
 #pragma unroll
-        for (int u = 0; u < RCVB; ++u) {
-          dst[u] = -1;
-          const int w = w0 + tid + nth * u;
-          const int q = w / KK, sl = w - (w / KK) * KK;
-          if (q < nfc) {
-            const int4 e = rcvtab[q];
-            const int kps = (((1 - nrd) ^ (e.z & 1)) + e.w + 1) & 1;
-            const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
-            if (e.y >= 0 && valid) {
-              off[u] = e.y + sl;
-              dst[u] = e.x + sl;
-              if (e.z & 1) wrapm |= 1u << u;
-              if (e.z & 2) sysm |= 1u << u;
-              const unsigned long long* src = ((e.z & 1) ? XB2 : XB1) + off[u];
-              v[u] = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < RCVB; ++u) {
-          if (dst[u] < 0) continue;
-          const bool w2 = (wrapm >> u) & 1u;
-          const unsigned want = w2 ? t2 : t1;
+        for (int h = 0; h < 2; ++h) {
+          if (!((vm >> (2 * u + h)) & 1u)) continue;
           unsigned spins = 0;
-          while ((unsigned)(v[u] >> 32) != want && !timed_out && !(a.debug & 1)) {
+          while ((unsigned)(v[u][h] >> 32) != want && !timed_out && !(a.debug & 1)) {
+            if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
+              atomicOr(a.err, 1u);
+              timed_out = true;
+            }
+            const unsigned long long* src = (w2 ? XB2 : XB1) + roff[u] + h;
+            v[u][h] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
+          }
+          Sd[rdst[u] + h] = __uint_as_float((unsigned)v[u][h]);
+        }
+      }
+      // pairs beyond the register-held ones (large tiles / deep columns), one
+      // word at a time
+      for (int w0 = RCVP * nth; w0 < nrcv; w0 += nth) {
+        const int w = w0 + tid;
+        const int q = w / HP, sl0 = 2 * (w - (w / HP) * HP);
+        if (q >= nfc) continue;
+        const int4 e = rcvtab[q];
+        if (e.y < 0) continue;
+        const int kps = (((1 - nrd) ^ (e.z & 1)) + e.w + 1) & 1;
+        const bool w2 = e.z & 1;
+        const unsigned want = w2 ? t2 : t1;
+        for (int h = 0; h < 2; ++h) {
+          const int sl = sl0 + h;
+          const bool valid = kps ? sl <= ((km - 1) >> 1) : (sl >= 1 && sl <= ((km - 2) >> 1) + 1);
+          if (!valid) continue;
+          const unsigned long long* src = (w2 ? XB2 : XB1) + e.y + sl;
+          unsigned long long x = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
+          unsigned spins = 0;
+          while ((unsigned)(x >> 32) != want && !timed_out && !(a.debug & 1)) {
             if (++spins > (1u << 24)) {
               atomicOr(a.err, 1u);
               timed_out = true;
             }
-            const unsigned long long* src = (w2 ? XB2 : XB1) + off[u];
-            v[u] = (SLAB && ((sysm >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
+            x = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
           }
-          Sd[dst[u]] = __uint_as_float((unsigned)v[u]);
+          Sd[e.x + sl] = __uint_as_float((unsigned)x);
         }
       }
     }
@@ -742,7 +750,7 @@ ResPlan plan_resident(const Geo& g, int device, int max_tiles) {
   }
   if (best == (size_t)-1) return pl;
   const int fmax = pl.ti_max > pl.tj_max ? pl.ti_max : pl.tj_max;
-  pl.fstride = (long long)fmax * pl.kk;
+  pl.fstride = (long long)fmax * ((pl.kk + 1) & ~1);  // even words per face column (16-byte pairs)
   pl.bstride = (4LL * pl.ni * pl.nj + 2LL * pl.nj) * pl.fstride;  // tile faces + ghost slots
   pl.xbuf = 4 * pl.bstride;
   pl.ok = true;
