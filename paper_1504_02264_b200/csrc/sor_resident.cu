@@ -110,6 +110,12 @@ __device__ __forceinline__ unsigned long long ld_ll_sys(const unsigned long long
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
   return w;
 }
+__device__ __forceinline__ void st_ll_pair(unsigned long long* a, unsigned long long x, unsigned long long y) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(a), "l"(x), "l"(y));
+}
+__device__ __forceinline__ void st_ll_pair_sys(unsigned long long* a, unsigned long long x, unsigned long long y) {
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(a), "l"(x), "l"(y));
+}
 __device__ __forceinline__ void ld_ll2(const unsigned long long* a, unsigned long long& x, unsigned long long& y) {
   // two LL words in one 16-byte load (each 8-byte element single-copy atomic)
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a));
@@ -312,6 +318,99 @@ __device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const 
     c += dq;
     if (t >= KT) {
       t -= KT;
+      ++c;
+    }
+  }
+  return acc;
+}
+
+// Boundary phase over slot PAIRS: unit w = (c - c0) * HP + j goes to thread
+// w % nth and updates the colour-nrd cells in slots 2j, 2j + 1 of column c
+// (one column decode per two cells, the bottom neighbour of the second cell
+// is the top one of the first), then publishes both words with one 16-byte
+// store (face columns have an even number of words; the word of a slot
+// holding no cell is never read by the receiver).
+template <bool PRESS, bool SLAB>
+__device__ __forceinline__ double update_flat2(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
+                                               const int2* __restrict__ pubcol, unsigned long long* X,
+                                               unsigned long long* XRw, unsigned long long* XRe, unsigned tag,
+                                               int c0, int c1, int HP, int nrd, int KK, int CW, int sI, int km) {
+  double acc = 0.0;
+  const int nth = RES_THREADS;
+  int c = c0 + (int)threadIdx.x / HP, j = (int)threadIdx.x - ((int)threadIdx.x / HP) * HP;
+  const int dq = nth / HP, dr = nth - (nth / HP) * HP;
+  float* Sc = S + nrd * KK;
+  const float* So = S + (1 - nrd) * KK;
+  const unsigned long long tagw = (unsigned long long)tag << 32;
+  while (c < c1) {
+    const unsigned ci = coltab[c];
+    const int cb = (int)(ci & CB_MASK);
+    const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
+    const int s0 = 2 * j;
+    // slot s holds k = 2 s + kp; a cell when 1 <= k <= km
+    const bool v0 = s0 + kp >= 1 && 2 * s0 + kp <= km;
+    const bool v1 = 2 * (s0 + 1) + kp <= km;
+    if (v0 || v1) {
+      const float* o = So + (cb + s0);  // other colour, same k as slot s0
+      float* ce = Sc + (cb + s0);
+      const float pc0 = ce[0], pc1 = ce[1];
+      const float pE0 = o[sI], pE1 = o[sI + 1];
+      float pW0 = o[-sI], pW1 = o[-sI + 1];
+      const float pN0 = o[CW], pN1 = o[CW + 1];
+      const float pS0 = o[-CW], pS1 = o[-CW + 1];
+      float pB0 = o[kp - 1];             // k - 1 of the first cell
+      const float pTB = o[kp];           // k + 1 of the first = k - 1 of the second
+      const float pT1 = o[kp + 1];
+      const float r0 = ce[2 * KK], r1 = ce[2 * KK + 1];
+      float pB1 = pTB;
+      if (PRESS) {
+        if (ci & (1u << 29)) {  // physical west: p[0] -> p[1]
+          pW0 = pc0;
+          pW1 = pc1;
+        }
+        if (2 * s0 + kp == 1) pB0 = pc0;  // bottom: p[.,.,0] -> p[.,.,1]
+      }
+      // sor.py:164-171: E, W, N, S, T, B summed left to right
+      float nb0 = a.w2l * pE0, nb1 = a.w2l * pE1;
+      nb0 = nb0 + a.w2s * pW0;
+      nb1 = nb1 + a.w2s * pW1;
+      nb0 = nb0 + a.w3l * pN0;
+      nb1 = nb1 + a.w3l * pN1;
+      nb0 = nb0 + a.w3s * pS0;
+      nb1 = nb1 + a.w3s * pS1;
+      nb0 = nb0 + a.w4l * pTB;
+      nb1 = nb1 + a.w4l * pT1;
+      nb0 = nb0 + a.w4s * pB0;
+      nb1 = nb1 + a.w4s * pB1;
+      // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+      const float rel0 = a.om * (a.cn1 * (nb0 - r0) - pc0);
+      const float rel1 = a.om * (a.cn1 * (nb1 - r1) - pc1);
+      const float np0 = v0 ? pc0 + rel0 : pc0;
+      const float np1 = v1 ? pc1 + rel1 : pc1;
+      if (v0) ce[0] = np0;
+      if (v1) ce[1] = np1;
+      const unsigned long long w0 = tagw | __float_as_uint(np0), w1 = tagw | __float_as_uint(np1);
+      const int2 pub = pubcol[c];  // a column lies on at most two faces
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = h ? pub.y : pub.x;
+        if (v < 0) continue;
+        if (!SLAB) {
+          st_ll_pair(X + (unsigned)(v + s0), w0, w1);
+        } else {
+          const unsigned off = (unsigned)((v & PUB_OFF) + s0);
+          if (v & PUB_RW) st_ll_pair_sys(XRw + off, w0, w1);
+          else if (v & PUB_RE) st_ll_pair_sys(XRe + off, w0, w1);
+          else st_ll_pair(X + off, w0, w1);
+        }
+      }
+      if (v0) acc += (double)rel0 * (double)rel0;
+      if (v1) acc += (double)rel1 * (double)rel1;
+    }
+    j += dr;
+    c += dq;
+    if (j >= HP) {
+      j -= HP;
       ++c;
     }
   }
@@ -638,7 +737,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
     unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
     if (!(a.debug & 2))
-      acc = update_flat<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KT, nrd, KK, CW, sI, km);
+      acc = update_flat2<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KKF >> 1, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!(a.debug & 2)) acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 5] = gtimer();
