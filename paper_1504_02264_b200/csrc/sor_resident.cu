@@ -9,12 +9,14 @@
 // L2, once per colour pass:
 //
 //   for pass n (colour nrd = n & 1):
-//     update the colour-nrd cells of the tile's BOUNDARY columns
-//     publish their colour-nrd values to a global face buffer, release flag
-//     update the colour-nrd cells of the tile's INTERIOR columns (this hides
-//       the latency of the publish / flag round trip)
-//     acquire-wait until every neighbour's flag >= n + 1
-//     copy the neighbours' published faces into the tile's halo columns
+//     receive: the neighbours' pass n-1 faces (self-validating LL words, one
+//       16-byte load per slot pair) into this tile's halo columns; barrier
+//     update the colour-nrd cells of the tile's BOUNDARY columns, two slots
+//       per work unit, publishing each pair of new values with one 16-byte
+//       store into the tile's face slots (or, on an x-slab edge, straight
+//       into the neighbour slab's ghost slot -- NVLink peer memory across GPUs)
+//     update the colour-nrd cells of the tile's INTERIOR columns while the
+//       published faces travel
 //
 // Layout ("colour split"): cell (i,j,k) lives in colour array
 // colour(i,j,k) = (i+j+k+1)&1 at slot k>>1 of its column, so for a fixed
@@ -24,9 +26,8 @@
 //   k = 2t + 2 - kp, centre slot t + 1 - kp, top slot t + 1, bottom slot t,
 // so every address is (column base + t + constant).
 //
-// Work items (column, t) are walked with an incremental decode (no integer
-// division in the pass loop) over a column table whose boundary columns come
-// first.  Halo slots take the colour of their storage position; for the
+// Work units are walked with an incremental decode (no integer division in
+// the pass loop) over a column table whose boundary columns come first.  Halo slots take the colour of their storage position; for the
 // periodic wrap with odd jm the source cell has the other colour, which is
 // exactly the reference's pre-pass snapshot of the y halo (the slot is only
 // refreshed after the pass that updated its source).
@@ -244,82 +245,6 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
     ++oth;
     ++tb;
     ++rr;
-  }
-  return acc;
-}
-
-// Flat walk for the boundary phase: item w = (c - c0) * KT + t goes to thread
-// w % nth, so a warp's lanes take consecutive slots of one column (rarely
-// two): the shared loads are conflict free and the publish stores of a
-// warp are consecutive words (coalesced).  Incremental (c, t) decode.
-template <bool PRESS, bool SLAB>
-__device__ __forceinline__ double update_flat(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
-                                              const int2* __restrict__ pubcol, unsigned long long* X,
-                                              unsigned long long* XRw, unsigned long long* XRe, unsigned tag,
-                                              int c0, int c1, int KT, int nrd, int KK, int CW, int sI, int km) {
-  double acc = 0.0;
-  const int nth = RES_THREADS;
-  int c = c0 + (int)threadIdx.x / KT, t = (int)threadIdx.x - ((int)threadIdx.x / KT) * KT;
-  const int dq = nth / KT, dr = nth - (nth / KT) * KT;
-  float* Sc = S + nrd * KK;
-  const float* So = S + (1 - nrd) * KK;
-  const unsigned long long tagw = (unsigned long long)tag << 32;
-  while (c < c1) {
-    const unsigned ci = coltab[c];
-    const int cb = (int)(ci & CB_MASK);
-    const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
-    const int k = 2 * t + 2 - kp;
-    if (k <= km) {
-      const int sl = t + 1 - kp;
-      const float* o = So + (cb + sl);  // other colour, same k
-      float* ce = Sc + (cb + sl);       // centre
-      const float pc = ce[0];
-      const float pE = o[sI];
-      float pW = o[-sI];
-      const float pN = o[CW];
-      const float pS = o[-CW];
-      const float pT = o[kp];           // slot t + 1
-      float pB = o[kp - 1];             // slot t
-      const float r = ce[2 * KK];
-      if (PRESS) {
-        if (ci & (1u << 29)) pW = pc;  // physical west: p[0] -> p[1]
-        if (k == 1) pB = pc;            // bottom: p[.,.,0] -> p[.,.,1]
-      }
-      // sor.py:164-171: E, W, N, S, T, B summed left to right
-      float nb = a.w2l * pE;
-      nb = nb + a.w2s * pW;
-      nb = nb + a.w3l * pN;
-      nb = nb + a.w3s * pS;
-      nb = nb + a.w4l * pT;
-      nb = nb + a.w4s * pB;
-      // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
-      const float rel = a.om * (a.cn1 * (nb - r) - pc);
-      const float np = pc + rel;
-      ce[0] = np;
-      const int2 pub = pubcol[c];  // a column lies on at most two faces
-      const unsigned long long w = tagw | __float_as_uint(np);
-      if (!SLAB) {
-        if (pub.x >= 0) st_ll_word(X + (unsigned)(pub.x + sl), w);
-        if (pub.y >= 0) st_ll_word(X + (unsigned)(pub.y + sl), w);
-      } else {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int v = h ? pub.y : pub.x;
-          if (v < 0) continue;
-          const unsigned o = (unsigned)((v & PUB_OFF) + sl);
-          if (v & PUB_RW) st_ll_sys(XRw + o, w);
-          else if (v & PUB_RE) st_ll_sys(XRe + o, w);
-          else st_ll_word(X + o, w);
-        }
-      }
-      acc += (double)rel * (double)rel;
-    }
-    t += dr;
-    c += dq;
-    if (t >= KT) {
-      t -= KT;
-      ++c;
-    }
   }
   return acc;
 }
