@@ -53,6 +53,9 @@ namespace lesb {
 constexpr int RES_THREADS = 512;
 constexpr int RES_WARPS = RES_THREADS / 32;
 constexpr int NST = 6;   // LESB_RES_TRACE stamps per pass
+#ifndef RES_RU
+#define RES_RU 4
+#endif
 constexpr int RCVP = 3;  // receive slot pairs each thread keeps in registers  // face values each thread has in flight while receiving
 
 struct ResPlan {
@@ -177,7 +180,7 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
   // Groups of RU cells: every load of the group is issued before the first
   // store (the colour-nrd stores never alias the other-colour and rhs loads,
   // which the compiler cannot prove), so RU point updates overlap.
-  constexpr int RU = 4;
+  constexpr int RU = RES_RU;
   for (; t + RU <= t1; t += RU) {
     float pc[RU], pE[RU], pW[RU], pN[RU], pS[RU], pT[RU], r[RU];
 #pragma unroll
@@ -211,7 +214,10 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
       cur[u] = pc[u] + rel;
       d[u] = (double)rel * (double)rel;
     }
-    acc += (d[0] + d[1]) + (d[2] + d[3]);
+    double gsum = 0.0;
+#pragma unroll
+    for (int u = 0; u < RU; ++u) gsum += d[u];
+    acc += gsum;
     pB = pT[RU - 1];
     cur += RU;
     oth += RU;
