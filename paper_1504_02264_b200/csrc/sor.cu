@@ -145,21 +145,42 @@ __global__ void __launch_bounds__(RB_NT) k_sor_rb(Geo g, float* __restrict__ p, 
 // (sor.py:206-246).
 constexpr int TW_BX = 32, TW_BY = 8, TW_NW = TW_BX * TW_BY / 32;
 
-template <int POL>
+// TW_R rows per thread (j, j + TW_BY, ...): src and dst never alias, so all
+// rows' loads go out together; UNI: scalar weights and 32-bit indexing.
+constexpr int TW_R = 4;
+template <int POL, bool UNI>
 __global__ void __launch_bounds__(TW_BX* TW_BY) k_sor_tw(Geo g, const float* __restrict__ src,
                                                          float* __restrict__ dst, const float* __restrict__ rhs,
                                                          SorC cf, float om, double* __restrict__ partials) {
   __shared__ double red[TW_NW];
   const int k = blockIdx.x * TW_BX + threadIdx.x + 1;
-  const int j = blockIdx.y * TW_BY + threadIdx.y + 1;
   const int i = blockIdx.z + 1;
+  float pc[TW_R], rel[TW_R];
+  long long cc[TW_R];
+  bool ok[TW_R];
+#pragma unroll
+  for (int q = 0; q < TW_R; ++q) {
+    const int j = (blockIdx.y * TW_R + q) * TW_BY + threadIdx.y + 1;
+    ok[q] = j <= g.jm && k <= g.km;
+    cc[q] = 0;
+    pc[q] = rel[q] = 0.0f;
+    if (!ok[q]) continue;
+    if (UNI) {
+      const int c = i * (int)g.si + j * g.sj + k;
+      cc[q] = c;
+      rel[q] = sor_point<POL, true, int>(g, src, rhs, cf, om, c, i, j, k, 0, pc[q]);
+    } else {
+      const long long c = cidx(g, i, j, k);
+      cc[q] = c;
+      rel[q] = sor_point<POL>(g, src, rhs, cf, om, c, i, j, k, 0, pc[q]);
+    }
+  }
   double acc = 0.0;
-  if (j <= g.jm && k <= g.km) {
-    const long long c = cidx(g, i, j, k);
-    float pc;
-    const float rel = sor_point<POL>(g, src, rhs, cf, om, c, i, j, k, 0, pc);
-    dst[c] = pc + rel;
-    acc = (double)rel * (double)rel;
+#pragma unroll
+  for (int q = 0; q < TW_R; ++q) {
+    if (!ok[q]) continue;
+    dst[cc[q]] = pc[q] + rel[q];
+    acc += (double)rel[q] * (double)rel[q];
   }
   const double s = block_sum<TW_NW>(acc, red);
   if (threadIdx.x == 0 && threadIdx.y == 0)
@@ -291,7 +312,7 @@ int sor_blocks_rb(const Geo& g) {
   return ((kh + bx - 1) / bx) * ((g.jm + by * RB_R - 1) / (by * RB_R)) * g.im;
 }
 int sor_blocks_tw(const Geo& g) {
-  return ((g.km + TW_BX - 1) / TW_BX) * ((g.jm + TW_BY - 1) / TW_BY) * g.im;
+  return ((g.km + TW_BX - 1) / TW_BX) * ((g.jm + TW_BY * TW_R - 1) / (TW_BY * TW_R)) * g.im;
 }
 
 void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, float om, int nrd, int policy,
@@ -318,10 +339,16 @@ void launch_rb_pass(const Geo& g, float* p, const float* rhs, const SorC& cf, fl
 
 void launch_tw_sweep(const Geo& g, const float* src, float* dst, const float* rhs, const SorC& cf, float om,
                      int policy, double* partials, cudaStream_t st) {
-  dim3 grid((g.km + TW_BX - 1) / TW_BX, (g.jm + TW_BY - 1) / TW_BY, g.im);
+  dim3 grid((g.km + TW_BX - 1) / TW_BX, (g.jm + TW_BY * TW_R - 1) / (TW_BY * TW_R), g.im);
   dim3 block(TW_BX, TW_BY);
-  if (policy == 1) k_sor_tw<1><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
-  else k_sor_tw<0><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+  const bool uni = cf.uni && !cf.cn1 && (long long)(g.im + 3) * g.si < (1LL << 31);
+  if (policy == 1) {
+    if (uni) k_sor_tw<1, true><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+    else k_sor_tw<1, false><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+  } else {
+    if (uni) k_sor_tw<0, true><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+    else k_sor_tw<0, false><<<grid, block, 0, st>>>(g, src, dst, rhs, cf, om, partials);
+  }
 }
 
 void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st) {

@@ -10,7 +10,8 @@ bracketed by CUDA events on the domain stream, with L2 flushed before it.
 
 Prints one JSON line: M cell-iterations/s, us per iteration, and the HBM
 roofline fraction at 12 B per cell and iteration (p read + write, rhs read;
-cn1 is a scalar).
+cn1 is a scalar).  --scheme twinned runs twinned (Jacobi) sweeps at omega 1.0
+(two sweeps per iteration; the same 12 B reference for comparability).
 """
 import argparse
 import json
@@ -32,6 +33,7 @@ ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--n-iter", type=int, default=50)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--halo", default="stored", choices=["stored", "press"])
+ap.add_argument("--scheme", default="redblack", choices=["redblack", "twinned"])
 a = ap.parse_args()
 im, jm, km = a.dims
 P.runtime.set_sor_path(a.path)
@@ -56,7 +58,9 @@ for r in range(a.reps + 1):
         flush.fill_(float(r))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    N.check(lib.lesb_sor_solve(h.h, a.n_iter, N.LESB_REDBLACK, 1.7, policy, N.dptr(res)), "sor_solve")
+    rb = a.scheme == "redblack"
+    N.check(lib.lesb_sor_solve(h.h, a.n_iter, N.LESB_REDBLACK if rb else N.LESB_TWINNED, 1.7 if rb else 1.0, policy,
+                               N.dptr(res)), "sor_solve")
     e1.record(stream)
     torch.cuda.synchronize()
     if r > 0:
@@ -67,8 +71,10 @@ peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.ex
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
 gbs = 12 * n * a.n_iter / (ms * 1e-3) / 1e9
 print(json.dumps({
-    "config": f"press-only {im}x{jm}x{km}, RB omega 1.7, {a.n_iter} iterations, halo {a.halo}",
-    "sor_kernel": {1: "k_sor_rb", 2: "k_sor_resident", 3: "k_sor_rbfused"}[lib.lesb_sor_path_in_use(h.h, 0)],
+    "config": (f"press-only {im}x{jm}x{km}, " + ("RB omega 1.7" if a.scheme == "redblack" else "TW omega 1.0") +
+               f", {a.n_iter} iterations, halo {a.halo}"),
+    "sor_kernel": ({1: "k_sor_rb", 2: "k_sor_resident", 3: "k_sor_rbfused"}[lib.lesb_sor_path_in_use(h.h, 0)]
+                   if a.scheme == "redblack" else "k_sor_tw"),
     "ms_per_solve": ms, "us_per_iteration": 1000 * ms / a.n_iter,
     "mcell_iter_per_s": n * a.n_iter / (ms * 1e-3) / 1e6,
     "roofline": {"bytes_per_cell_iteration": 12, "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"],
