@@ -42,6 +42,9 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
@@ -67,6 +70,7 @@ struct ResPlan {
   long long fstride;  // words per face slot
   long long bstride;  // words per ring buffer: ntiles * 4 faces + 2 * nj ghost slots
   long long xbuf;   // words of the face exchange buffer (4 ring buffers)
+  int pad[2][2];    // row pad by (TI == ti_max ? 0 : 1, TJ == tj_max ? 0 : 1)
   bool ok;
 };
 
@@ -140,7 +144,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__host__ __device__ __forceinline__ int row_pad(int cw) { return (32 - ((4 * cw) & 31)) & 31; }
+constexpr int ROW_PAD_MAX = 31;  // row padding of the column grid (chosen per tile shape by the plan)
 
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
 
@@ -401,10 +405,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   // column stride along i, padded so that sI = (TJ - 2) CW (mod 32): the
   // interior columns then sit at CW * (ordinal) + const modulo the 32 banks,
   // and a warp's lanes on 32 consecutive interior columns never conflict
-  const int PADI = row_pad(CW);
+  // column stride along i: (TJ + 2) CW plus the row pad the plan chose for
+  // this tile shape (fewest shared-memory bank conflicts in the interior runs)
+  const int PADI = pl.pad[TI == pl.ti_max ? 0 : 1][TJ == pl.tj_max ? 0 : 1];
   const int sI = (TJ + 2) * CW + PADI;
   float* S = smem;                           // [ti+2][sI]: columns of [4][KK] (+1), rows padded
-  const long long s_floats = (long long)(pl.ti_max + 2) * ((pl.tj_max + 2) * CW + PADI);
+  const long long s_floats = (long long)(pl.ti_max + 2) * ((pl.tj_max + 2) * CW + ROW_PAD_MAX);
   unsigned* coltab = reinterpret_cast<unsigned*>(smem + ((s_floats + 3) & ~3LL));   // [TI*TJ]
   int2* pubcol = reinterpret_cast<int2*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
   int4* rcvtab = reinterpret_cast<int4*>(pubcol + ((pl.ti_max * pl.tj_max + 1) & ~1));  // [2TI+2TJ]
@@ -741,14 +747,66 @@ static int g_max_smem = -1;
 
 static size_t plan_smem(int tim, int tjm, int kk) {
   const int cw = 4 * kk + 1;
-  const size_t arrays = 4ull * ((((size_t)cw * (tjm + 2) + row_pad(cw)) * (tim + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
+  const size_t arrays = 4ull * ((((size_t)cw * (tjm + 2) + ROW_PAD_MAX) * (tim + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
   const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
   const size_t pubcol = 8ull * ((tim * tjm + 1) & ~1);
   const size_t rcvtab = 16ull * 2 * (tim + tjm);
   return arrays + coltab + pubcol + rcvtab;
 }
 
+// Shared-memory bank load of the interior runs for a row pad: warps of 32
+// consecutive interior columns (the unit order of update_phase) touch
+// column base + (1 - kp) (kp alternates with the column parity); the sum
+// over warps and both colours of the most-loaded bank.
+static int interior_bank_load(int TI, int TJ, int kk, int pad) {
+  const int cw = 4 * kk + 1, sI = (TJ + 2) * cw + pad;
+  const int nj = TJ - 2, nint = (TI - 2) * nj;
+  int load = 0;
+  for (int nrd = 0; nrd < 2; ++nrd)
+    for (int w0 = 0; w0 < nint; w0 += 32) {
+      int cnt[32] = {0};
+      int mx = 0;
+      for (int r = w0; r < nint && r < w0 + 32; ++r) {
+        const int li = 2 + r / nj, lj = 2 + r % nj;
+        const int kp = (nrd + ((li + lj) & 1) + 1) & 1;
+        const int b = (li * sI + lj * cw + nrd * kk + (1 - kp)) & 31;
+        mx = ++cnt[b] > mx ? cnt[b] : mx;
+      }
+      load += mx;
+    }
+  return load;
+}
+
+static int best_row_pad(int TI, int TJ, int kk) {
+  if (TI <= 2 || TJ <= 2) return 0;
+  int best = 0, bl = 1 << 30;
+  for (int pad = 0; pad <= ROW_PAD_MAX; ++pad) {
+    const int l = interior_bank_load(TI, TJ, kk, pad);
+    if (l < bl) {
+      bl = l;
+      best = pad;
+    }
+  }
+  return best;
+}
+
+static ResPlan plan_resident_uncached(const Geo& g, int device, int max_tiles);
+
+// plans are pure functions of (im, jm, km, max_tiles) on one GPU model; the
+// row-pad search makes them worth caching (they are asked for on every solve)
 ResPlan plan_resident(const Geo& g, int device, int max_tiles) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, ResPlan> cache;
+  const auto key = std::make_tuple(g.im, g.jm, g.km, max_tiles);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  ResPlan pl = plan_resident_uncached(g, device, max_tiles);
+  cache.emplace(key, pl);
+  return pl;
+}
+
+static ResPlan plan_resident_uncached(const Geo& g, int device, int max_tiles) {
   ResPlan pl{};
   pl.ok = false;
   if (g_num_sms < 0) {
@@ -783,6 +841,8 @@ ResPlan plan_resident(const Geo& g, int device, int max_tiles) {
   pl.fstride = (long long)fmax * ((pl.kk + 1) & ~1);  // even words per face column (16-byte pairs)
   pl.bstride = (4LL * pl.ni * pl.nj + 2LL * pl.nj) * pl.fstride;  // tile faces + ghost slots
   pl.xbuf = 4 * pl.bstride;
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) pl.pad[a][b] = best_row_pad(pl.ti_max - a, pl.tj_max - b, pl.kk);
   pl.ok = true;
   return pl;
 }
