@@ -45,7 +45,14 @@ __device__ __forceinline__ float sor_point(const Geo& g, const float* __restrict
   const IDX si = (IDX)g.si, sj = (IDX)g.sj;
   const float pc = p[c];
   float pE, pW, pN, pS, pT, pB;
-  if (POL == 1) {
+  if (POL == 3) {  // press, cell away from the x and y faces: only the k remaps
+    pE = p[c + si];
+    pW = p[c - si];
+    pN = p[c + sj];
+    pS = p[c - sj];
+    pT = (k == g.km) ? 0.0f : p[c + 1];
+    pB = (k == 1) ? pc : p[c - 1];
+  } else if (POL == 1) {
     pE = (i == g.im && g.east_bc) ? 0.0f : p[c + si];
     pW = (i == 1 && g.west_bc) ? pc : p[c - si];
     pN = (j == g.jm && !y_stored) ? p[c - (IDX)(g.jm - 1) * sj] : p[c + sj];
@@ -114,7 +121,12 @@ __global__ void __launch_bounds__(RB_NT) k_sor_rb(Geo g, float* __restrict__ p, 
     if (UNI) {
       const int c = i * (int)g.si + j * g.sj + k;
       cc[q] = c;
-      rel[q] = sor_point<POL, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc[q]);
+      // press: rows away from the x and y faces need only the k remaps
+      // (block-uniform in i, row-uniform in j)
+      if (POL == 1 && i > 1 && i < g.im && j > 1 && j < g.jm)
+        rel[q] = sor_point<3, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc[q]);
+      else
+        rel[q] = sor_point<POL, true, int>(g, p, rhs, cf, om, c, i, j, k, y_stored, pc[q]);
     } else {
       const long long c = cidx(g, i, j, k);
       cc[q] = c;
@@ -168,7 +180,10 @@ __global__ void __launch_bounds__(TW_BX* TW_BY) k_sor_tw(Geo g, const float* __r
     if (UNI) {
       const int c = i * (int)g.si + j * g.sj + k;
       cc[q] = c;
-      rel[q] = sor_point<POL, true, int>(g, src, rhs, cf, om, c, i, j, k, 0, pc[q]);
+      if (POL == 1 && i > 1 && i < g.im && j > 1 && j < g.jm)  // press away from the x / y faces
+        rel[q] = sor_point<3, true, int>(g, src, rhs, cf, om, c, i, j, k, 0, pc[q]);
+      else
+        rel[q] = sor_point<POL, true, int>(g, src, rhs, cf, om, c, i, j, k, 0, pc[q]);
     } else {
       const long long c = cidx(g, i, j, k);
       cc[q] = c;
