@@ -493,6 +493,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   // column).  Every element is an asynchronous 4-byte copy (cp.async, zero-fill
   // where the value is a constant 0), so all of a thread's loads are in flight
   // at once instead of one L2 round trip per column chunk. ----
+  // LESB_RES_TRACE: per-tile stamps of the phases around the pass loop
+  unsigned long long* tx = a.trace ? a.trace + ((long long)ntiles * 2 * a.n_iter) * NST + (long long)tile * 8 : nullptr;
+  if (tx && tid == 0) tx[0] = gtimer();
   const unsigned sm_s = (unsigned)__cvta_generic_to_shared(S);
   const int ncol_h = (TI + 2) * (TJ + 2);
   for (int col = warp; col < ncol_h; col += RES_WARPS) {
@@ -597,6 +600,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   bool timed_out = false;
 
   unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * NST : nullptr;
+  if (tx && tid == 0) tx[1] = gtimer();
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
     if (tr && tid == 0) tr[NST * n + 0] = gtimer();
@@ -684,6 +688,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   }
   __syncthreads();
 
+  if (tx && tid == 0) tx[2] = gtimer();
   // ---- write the tile back (warp per column); press: closed-form halo ----
   unsigned bad = 0;
   for (int c = warp; c < ncol; c += RES_WARPS) {
@@ -721,7 +726,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   if (a.pflags) flag_or(a.pflags, bad);
 
   // ---- residuals: tile b sums iteration b over tiles and warps in a fixed order ----
+  if (tx && tid == 0) tx[3] = gtimer();
   cg::this_grid().sync();
+  if (tx && tid == 0) tx[4] = gtimer();
   // fresh tags for the next launch (a group's slabs share one epoch word)
   if (tid == 0 && blockIdx.x == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);
   const int per_pass = ntiles * RES_WARPS;
@@ -737,6 +744,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     }
     if (tid == 0) a.res[it] = tot;
   }
+  if (tx && tid == 0) tx[5] = gtimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -932,7 +940,7 @@ cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st) {
   grp.n = 1;
   grp.tps = pl.ni * pl.nj;
   static const bool trace = getenv("LESB_RES_TRACE") != nullptr;
-  const size_t tneed = (size_t)grp.tps * 2 * c.n_iter * NST;
+  const size_t tneed = (size_t)grp.tps * 2 * c.n_iter * NST + (size_t)grp.tps * 8;  // + per-tile phase stamps
   if (trace) {
     if (g_tcap < tneed) {
       if (g_tbuf) cudaFree(g_tbuf);

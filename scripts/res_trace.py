@@ -18,12 +18,12 @@ res = np.zeros(50)
 for _ in range(3):
     N.check(lib.lesb_press(h.h, 50, 0, 1.7, N.dptr(res)), "press")
 NST = 6
-buf = np.zeros(200 * 100 * NST, np.uint64)
+buf = np.zeros(200 * 100 * NST + 200 * 8, np.uint64)
 fn = lib.lesb_debug_resident_trace
 fn.restype = ctypes.c_longlong
 n = fn(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), buf.size)
-nt = n // (100 * NST)
-t = buf[:n].reshape(nt, 100, NST).astype(np.int64)
+nt = n // (100 * NST + 8)
+t = buf[:nt * 100 * NST].reshape(nt, 100, NST).astype(np.int64)
 t = t - t[:, 0, 0].min()
 names = ["recv+barrier", "boundary", "barrier", "publish", "interior"]
 d = [(t[:, :, q + 1] - t[:, :, q]) / 1e3 for q in range(NST - 1)]
@@ -37,3 +37,12 @@ print("start skew across tiles at pass 50 (us): %.2f" % ((t[:, 50, 0].max() - t[
 comp = sum(d[1:])[:, 2:].mean(1)
 order = np.argsort(comp)
 print("per-tile work after receive (us): min %.2f median %.2f max %.2f" % (comp.min(), np.median(comp), comp.max()))
+ext = buf[nt * 100 * NST: nt * 100 * NST + nt * 8].reshape(nt, 8).astype(np.int64)
+if ext[:, 5].max() > 0:
+    t00 = ext[:, 0].min()
+    e = (ext[:, :6] - t00) / 1e3
+    print("phases around the pass loop (us, mean over tiles): entry->loop %.2f  loop %.2f  write-back %.2f  "
+          "grid sync %.2f  residuals %.2f  (kernel span %.2f)" % (
+              (e[:, 1] - e[:, 0]).mean(), (e[:, 2] - e[:, 1]).mean(), (e[:, 3] - e[:, 2]).mean(),
+              (e[:, 4] - e[:, 3]).mean(), (e[:, 5] - e[:, 4]).mean(), e[:, 5].max() - e[:, 0].min()))
+
