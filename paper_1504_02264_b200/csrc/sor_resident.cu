@@ -103,10 +103,6 @@ struct ResArgs {
 // tag of its pass in one 64-bit word, written and read with single-copy-atomic
 // 64-bit accesses, so a reader that sees the right tag also sees the right
 // value -- no fences, counters or flag round trips.
-__device__ __forceinline__ void st_ll(unsigned long long* a, float v, unsigned tag) {
-  const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
-}
 __device__ __forceinline__ void st_ll_word(unsigned long long* a, unsigned long long w) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w));
 }
@@ -266,7 +262,7 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
 // store (face columns have an even number of words; the word of a slot
 // holding no cell is never read by the receiver).
 template <bool PRESS, bool SLAB>
-__device__ __forceinline__ double update_flat2(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
+__device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
                                                const int2* __restrict__ pubcol, unsigned long long* X,
                                                unsigned long long* XRw, unsigned long long* XRe, unsigned tag,
                                                int c0, int c1, int HP, int nrd, int KK, int CW, int sI, int km) {
@@ -678,7 +674,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
     unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
     if (!(a.debug & 2))
-      acc = update_flat2<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KKF >> 1, nrd, KK, CW, sI, km);
+      acc = update_boundary<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KKF >> 1, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!(a.debug & 2)) acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 5] = gtimer();
