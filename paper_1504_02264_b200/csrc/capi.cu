@@ -208,30 +208,44 @@ void set_spacing_info(lesb_domain* h, const float* dx, const float* dy, const fl
 void clear_graphs(lesb_domain* h);
 
 bool map_slab_peers(lesb_domain* h) {
+  // Every rank takes part in both collectives whatever happens locally, and
+  // the peers are used only when every rank mapped both of its neighbours:
+  // a partial mapping would leave ranks on different solver paths (with
+  // different NCCL exchange sequences).
   const int nr = h->link.nranks, r = h->link.rank;
-  cudaIpcMemHandle_t mine;
-  if (cudaIpcGetMemHandle(&mine, h->xbuf) != cudaSuccess) return false;
-  // the handle plus this slab's plan signature: (im, jm, km, buffer words)
   struct Rec {
     cudaIpcMemHandle_t h;
-    long long im, jm, km, words;
-  } rec{mine, h->g.im, h->g.jm, h->g.km, resident_xbuf_words(h->g, h->device)};
+    long long im, jm, km, words, ok;
+  } rec{};
+  rec.ok = cudaIpcGetMemHandle(&rec.h, h->xbuf) == cudaSuccess;
+  rec.im = h->g.im;
+  rec.jm = h->g.jm;
+  rec.km = h->g.km;
+  rec.words = resident_xbuf_words(h->g, h->device);
   void* d = nullptr;
-  if (cudaMalloc(&d, sizeof(Rec) * (nr + 1)) != cudaSuccess) return false;
+  if (cudaMalloc(&d, sizeof(Rec) * (nr + 1) + sizeof(int) * 2) != cudaSuccess) return false;
   std::vector<Rec> all(nr);
+  int* flag = reinterpret_cast<int*>((char*)d + sizeof(Rec) * (nr + 1));
   bool ok = cudaMemcpy((char*)d + sizeof(Rec) * nr, &rec, sizeof(Rec), cudaMemcpyHostToDevice) == cudaSuccess &&
             ncclAllGather((char*)d + sizeof(Rec) * nr, d, sizeof(Rec), ncclChar, h->link.comm, h->st) == ncclSuccess &&
             cudaStreamSynchronize(h->st) == cudaSuccess &&
             cudaMemcpy(all.data(), d, sizeof(Rec) * nr, cudaMemcpyDeviceToHost) == cudaSuccess;
-  cudaFree(d);
-  if (!ok) return false;
-  for (int q = 0; q < nr; ++q)
-    if (all[q].im != rec.im || all[q].jm != rec.jm || all[q].km != rec.km || all[q].words != rec.words) return false;
+  for (int q = 0; ok && q < nr; ++q)
+    ok = all[q].ok && all[q].im == rec.im && all[q].jm == rec.jm && all[q].km == rec.km && all[q].words == rec.words;
   void* w = nullptr;
   void* e = nullptr;
-  if (r > 0 && cudaIpcOpenMemHandle(&w, all[r - 1].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return false;
-  if (r < nr - 1 && cudaIpcOpenMemHandle(&e, all[r + 1].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+  if (ok && r > 0) ok = cudaIpcOpenMemHandle(&w, all[r - 1].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+  if (ok && r < nr - 1) ok = cudaIpcOpenMemHandle(&e, all[r + 1].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+  // collective decision: min over ranks of "mapped"
+  int mine = ok ? 1 : 0, every = 0;
+  const bool agreed = cudaMemcpy(flag, &mine, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+                      ncclAllReduce(flag, flag + 1, 1, ncclInt, ncclMin, h->link.comm, h->st) == ncclSuccess &&
+                      cudaStreamSynchronize(h->st) == cudaSuccess &&
+                      cudaMemcpy(&every, flag + 1, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(d);
+  if (!agreed || !every) {
     if (w) cudaIpcCloseMemHandle(w);
+    if (e) cudaIpcCloseMemHandle(e);
     return false;
   }
   h->peer_w = w;
