@@ -391,10 +391,12 @@ cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omeg
   mark(0);
   launch_velnw_bondv1(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->inflow_d, h->ub, h->vb, h->wb,
                       flags, h->st);
-  if (h->link.comm) {  // x-slab: velocity halos after velnw + bondv1
+  if (h->link.comm) {  // x-slab: velocity halos after velnw + bondv1, one NCCL group
+    ncclGroupStart();
     nccl_exchange(h, h->ub, 2, h->st);
     nccl_exchange(h, h->vb, 2, h->st);
     nccl_exchange(h, h->wb, 2, h->st);
+    ncclGroupEnd();
   }
   mark(1);
   launch_fused_rhs(h->g, h->spac(), h->ub, h->vb, h->wb, h->mask, h->fgh, h->fgh_old, h->u, h->v, h->w, h->rhs,
