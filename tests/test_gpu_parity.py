@@ -197,6 +197,33 @@ def test_step_against_oracle_odd_shapes(P):
                 assert bits_equal(getattr(fs, n), getattr(o, n)), ((im, jm, km), scheme, s, n)
 
 
+@pytest.mark.parametrize("dims", [(36, 36, 600), (48, 40, 400), (30, 74, 257)])
+def test_deep_columns_against_oracle(P, dims, request):
+    """Deep columns on grids the resident solver takes: 3x3-class tiles of
+    km/2 slot pairs per face column overflow the receive descriptors each
+    thread keeps in registers, so the per-pass decoded receive walk runs too
+    (and odd km on the last shape)."""
+    from oracle import les_oracle as O
+    from paper_1504_02264_b200 import _native as N
+
+    im, jm, km = dims
+    st = gi.random_state(im, jm, km, seed=km, vel_scale=0.2)
+    inflow = gi.random_inflow(km, seed=7)
+    fs = dstate(P, st)
+    if request.node.callspec.params["P"] == 0:
+        h = fs.handle()
+        fs._ensure_coeffs(h)
+        assert N.load().lesb_sor_path_in_use(h.h, 0) == 2, dims  # resident
+    o = O.OState.zeros(im, jm, km)
+    for n in FIELDS + ("mask", "dx1", "dy1", "dzn"):
+        getattr(o, n)[...] = st[n]
+    for s in range(2):
+        P.les.step(fs, P.WindProfile(*inflow), n_iter=9, scheme=P.Scheme.REDBLACK)
+        O.step(o, *inflow, n_iter=9, scheme="redblack")
+        for n in FIELDS:
+            assert bits_equal(getattr(fs, n), getattr(o, n)), (dims, s, n)
+
+
 def test_press_150_anchors(P):
     """press-only 150x150x90, h=1, rng(0) rhs, 50 iterations."""
     rec = META.get("press150")
