@@ -81,3 +81,64 @@ def test_long_run_slabs_bitwise(nslabs, mode, monkeypatch):
             assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (nslabs, mode, n)
     finally:
         grp.close()
+
+
+def run_to_blowup(stepper, limit):
+    """Steps until NumericsError; returns (failing step, 1-based; stage)."""
+    import paper_1504_02264_b200 as P
+
+    done = 0
+    with pytest.raises(P.NumericsError) as err:
+        while done < limit:
+            stepper()
+            done += 1
+    return done + 1, err.value.stage
+
+
+@pytest.mark.parametrize("dims,nslabs,want", [((150, 150, 90), 2, (54, "velfg")),
+                                              ((600, 600, 90), 4, None)])
+def test_km90_blowup_step_and_stage(dims, nslabs, want):
+    """the building-free km=90 flow is not finite in the
+    reference dynamics (probe P10: 150x150x90 fails in velfg at step 54).  One
+    domain reaches the reference's failing step and stage, and an x-slab
+    decomposition fails at the same step and stage (600x600x90: the strong-
+    scaling grid, whose failing step the reference did not record)."""
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200.slabs import SlabGroup
+
+    st, g = make(P, dims)
+    inflow = P.WindProfile(*gi.default_inflow(dims[2]))
+    fs = P.FlowState.create(g, dt=0.5, vn=0.8, cs=0.14)
+    one = run_to_blowup(lambda: P.les.step(fs, inflow), 200)
+    if want is not None:
+        assert one == want
+    grp = SlabGroup(g, nslabs, dt=0.5, vn=0.8, cs=0.14)
+    try:
+        grp.upload(st)
+        assert run_to_blowup(lambda: grp.step(inflow), 200) == one
+    finally:
+        grp.close()
+
+
+def test_weak_scaling_long_run_slabs_bitwise():
+    """Config 5(c): 300x300x32 per GPU x 1000 steps, here two slabs (global
+    600x300x32) on one device against the single domain, bitwise."""
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200.slabs import SlabGroup
+
+    dims, n_steps = (600, 300, 32), 1000
+    st, g = make(P, dims)
+    inflow = P.WindProfile(*gi.default_inflow(dims[2]))
+    fs = P.FlowState.create(g, dt=0.5, vn=0.8, cs=0.14)
+    assert P.les.run_steps(fs, inflow, n_steps) == n_steps
+    grp = SlabGroup(g, 2, dt=0.5, vn=0.8, cs=0.14)
+    try:
+        grp.upload(st)
+        for _ in range(n_steps):
+            grp.step(inflow)
+        for n in ("u", "v", "w", "p", "fgh", "fgh_old"):
+            a, b = grp.gather(n), np.array(getattr(fs, n))
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), n
+        assert np.isfinite(np.array(fs.u)).all()
+    finally:
+        grp.close()
