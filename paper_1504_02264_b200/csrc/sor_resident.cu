@@ -91,7 +91,7 @@ struct ResArgs {
   unsigned long long* peer_w;
   unsigned long long* peer_e;
   unsigned* epoch;   // launch counter: tags of this launch are unique across launches
-  double* partials;  // [2 n_iter][ntiles][RES_WARPS] per-warp residual partials
+  double* partials;  // [n_iter][ntiles][RES_WARPS] per-warp residual partials (both colour passes)
   double* res;       // [n_iter] residual per iteration
   unsigned* pflags;  // stage flag word (F_PRESS) or nullptr
   unsigned* err;     // set when a neighbour wait times out
@@ -265,11 +265,11 @@ template <bool PRESS, bool SLAB>
 __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
                                                const int2* __restrict__ pubcol, unsigned long long* X,
                                                unsigned long long* XRw, unsigned long long* XRe, unsigned tag,
-                                               int c0, int c1, int HP, int nrd, int KK, int CW, int sI, int km) {
+                                               int c, int j, int dq, int dr, int c1, int HP, int nrd, int KK,
+                                               int CW, int sI, int km) {
+  // (c, j): this thread's first unit; (dq, dr): RES_THREADS units on, in
+  // (columns, pairs) -- pass invariants, decoded once before the pass loop
   double acc = 0.0;
-  const int nth = RES_THREADS;
-  int c = c0 + (int)threadIdx.x / HP, j = (int)threadIdx.x - ((int)threadIdx.x / HP) * HP;
-  const int dq = nth / HP, dr = nth - (nth / HP) * HP;
   float* Sc = S + nrd * KK;
   const float* So = S + (1 - nrd) * KK;
   const unsigned long long tagw = (unsigned long long)tag << 32;
@@ -353,18 +353,24 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
 // u % nth.  Column-fastest numbering puts a warp's lanes in consecutive
 // columns at the same slot offset; with the odd column stride their shared
 // addresses fall in distinct banks.
+// (g, cc): the segment and column of this thread's first run; (dg, dcc):
+// RES_THREADS runs on -- decoded once before the pass loop.
 template <bool PRESS>
 __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
-                                               int c0, int c1, int nseg, int L, int KT, int nrd, int KK, int CW,
-                                               int sI, int km) {
+                                               int c0, int c1, int nseg, int g, int cc, int dg, int dcc, int L,
+                                               int KT, int nrd, int KK, int CW, int sI, int km) {
   double acc = 0.0;
   const int ncc = c1 - c0;
-  const int nunits = ncc * nseg;
-  for (int u = threadIdx.x; u < nunits; u += RES_THREADS) {
-    const int g = u / ncc, cc = u - g * ncc;
+  while (g < nseg) {
     const int t0 = g * L;
     const int t1 = min(t0 + L, KT);
     acc += update_run<PRESS>(a, S, coltab[c0 + cc], t0, t1, nrd, KK, CW, sI, km);
+    g += dg;
+    cc += dcc;
+    if (cc >= ncc) {
+      cc -= ncc;
+      ++g;
+    }
   }
   return acc;
 }
@@ -555,6 +561,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   const int nint = ncol - nbnd;
   const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
   const int L_i = (KT + nseg_i - 1) / nseg_i;
+  // pass-invariant decode of this thread's first interior run / boundary pair
+  const int nint1 = max(nint, 1);
+  const int ig0 = nint > 0 ? tid / nint1 : nseg_i, icc0 = tid - (tid / nint1) * nint1;
+  const int idg = nth / nint1, idcc = nth - idg * nint1;
+  const int HPb = KKF >> 1;
+  const int bc0 = tid / HPb, bj0 = tid - bc0 * HPb, bdq = nth / HPb, bdr = nth - bdq * HPb;
   // receive walk over slot PAIRS (face column q, slots sl, sl + 1; sl even):
   // pair w = tid + nth u, one 16-byte load each (two LL words).  The first
   // RCVP pairs of every thread keep their descriptors in registers for the
@@ -594,6 +606,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     }
   }
   bool timed_out = false;
+  double acc = 0.0;
 
   unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * NST : nullptr;
   if (tx && tid == 0) tx[1] = gtimer();
@@ -670,17 +683,21 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     if (tr && tid == 0) tr[NST * n + 1] = gtimer();
     unsigned long long* X = a.xbuf + (n & 3) * bstride + (long long)tile * tstride;
     const unsigned tag = tag0 + (unsigned)(n + 2);
-    double acc = 0.0;
+    if (nrd == 0) acc = 0.0;  // one residual per iteration: both colour passes
     unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
     unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
     if (!(a.debug & 2))
-      acc = update_boundary<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, 0, nbnd, KKF >> 1, nrd, KK, CW, sI, km);
+      acc += update_boundary<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, bc0, bj0, bdq, bdr, nbnd, HPb, nrd,
+                                         KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
-    if (!(a.debug & 2)) acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, L_i, KT, nrd, KK, CW, sI, km);
+    if (!(a.debug & 2))
+      acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, idg, idcc, L_i, KT, nrd, KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 5] = gtimer();
+    if (nrd == 1) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if (lane == 0) a.partials[((long long)n * ntiles + tile) * RES_WARPS + warp] = acc;
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (lane == 0) a.partials[((long long)(n >> 1) * ntiles + tile) * RES_WARPS + warp] = acc;
+    }
   }
   __syncthreads();
 
@@ -729,16 +746,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   if (tid == 0 && blockIdx.x == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);
   const int per_pass = ntiles * RES_WARPS;
   for (int it = tile; it < a.n_iter; it += ntiles) {
-    double tot = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-      const double* q = a.partials + (long long)(2 * it + pass) * per_pass;
-      double v = 0.0;
-      for (int b = tid; b < per_pass; b += nth) v += q[b];
-      v = block_sum<RES_WARPS>(v, red);
-      __syncthreads();
-      tot += v;
-    }
-    if (tid == 0) a.res[it] = tot;
+    const double* q = a.partials + (long long)it * per_pass;
+    double v = 0.0;
+    for (int b = tid; b < per_pass; b += nth) v += q[b];
+    v = block_sum<RES_WARPS>(v, red);
+    __syncthreads();
+    if (tid == 0) a.res[it] = v;
   }
   if (tx && tid == 0) tx[5] = gtimer();
 }
