@@ -355,16 +355,34 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
 // addresses fall in distinct banks.
 // (g, cc): the segment and column of this thread's first run; (dg, dcc):
 // RES_THREADS runs on -- decoded once before the pass loop.
-template <bool PRESS>
+// mid() runs once, part-way through the thread's first run (or first, when
+// the thread has none): it issues the next pass's receive loads, so their
+// L2 round trip overlaps the rest of the interior.
+#ifndef RES_MID
+#define RES_MID 1
+#endif
+template <bool PRESS, class F>
 __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
                                                int c0, int c1, int nseg, int g, int cc, int dg, int dcc, int L,
-                                               int KT, int nrd, int KK, int CW, int sI, int km) {
+                                               int KT, int nrd, int KK, int CW, int sI, int km, F&& mid) {
   double acc = 0.0;
   const int ncc = c1 - c0;
+  bool issued = false;
   while (g < nseg) {
     const int t0 = g * L;
     const int t1 = min(t0 + L, KT);
-    acc += update_run<PRESS>(a, S, coltab[c0 + cc], t0, t1, nrd, KK, CW, sI, km);
+    const unsigned ci = coltab[c0 + cc];
+    if (!issued) {
+      constexpr int RU = RES_RU;
+      const int h = (t1 - t0) >> 1;
+      const int tm = min(t1, t0 + (RES_MID ? (h + RU - 1) / RU * RU : h / RU * RU));
+      acc += update_run<PRESS>(a, S, ci, t0, tm, nrd, KK, CW, sI, km);
+      mid();
+      issued = true;
+      acc += update_run<PRESS>(a, S, ci, tm, t1, nrd, KK, CW, sI, km);
+    } else {
+      acc += update_run<PRESS>(a, S, ci, t0, t1, nrd, KK, CW, sI, km);
+    }
     g += dg;
     cc += dcc;
     if (cc >= ncc) {
@@ -372,6 +390,7 @@ __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const
       ++g;
     }
   }
+  if (!issued) mid();
   return acc;
 }
 
@@ -610,6 +629,22 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
 
   unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * NST : nullptr;
   if (tx && tid == 0) tx[1] = gtimer();
+  // the receive loads of pass n (register-held pairs), issued during pass n-1
+  unsigned long long v[RCVP][2];
+  auto issue_receive = [&](int n) {
+    if (a.debug & 4) return;
+    const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
+    const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
+    const unsigned vm = (n & 1) ? rval1 : rval0;
+#pragma unroll
+    for (int u = 0; u < RCVP; ++u)
+      if ((vm >> (2 * u)) & 3u) {
+        const unsigned long long* src = (((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u];
+        if (SLAB && ((rsys >> u) & 1u)) ld_ll2_sys(src, v[u][0], v[u][1]);
+        else ld_ll2(src, v[u][0], v[u][1]);
+      }
+  };
+  issue_receive(0);
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
     if (tr && tid == 0) tr[NST * n + 0] = gtimer();
@@ -623,14 +658,6 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
       float* Sd = S + (1 - nrd) * KK;
       const unsigned vm = nrd ? rval1 : rval0;
-      unsigned long long v[RCVP][2];
-#pragma unroll
-      for (int u = 0; u < RCVP; ++u)
-        if ((vm >> (2 * u)) & 3u) {
-          const unsigned long long* src = (((rwrap >> u) & 1u) ? XB2 : XB1) + roff[u];
-          if (SLAB && ((rsys >> u) & 1u)) ld_ll2_sys(src, v[u][0], v[u][1]);
-          else ld_ll2(src, v[u][0], v[u][1]);
-        }
 #pragma unroll
       for (int u = 0; u < RCVP; ++u) {
         const bool w2 = (rwrap >> u) & 1u;
@@ -691,7 +718,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
                                          KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!(a.debug & 2))
-      acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, idg, idcc, L_i, KT, nrd, KK, CW, sI, km);
+      acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, idg, idcc, L_i, KT, nrd, KK, CW, sI, km,
+                                 [&] {
+                                   if (n + 1 < 2 * a.n_iter) issue_receive(n + 1);
+                                 });
     if (tr && tid == 0) tr[NST * n + 5] = gtimer();
     if (nrd == 1) {
 #pragma unroll
