@@ -6,6 +6,9 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > 
 timeout 600 python -m pytest tests -q -m gpu > gpurun_out/ev/pytest_gpu.txt 2>&1; tail -3 gpurun_out/ev/pytest_gpu.txt
 timeout 900 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.err; cat gpurun_out/ev/bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ev/bench_ref.json 2>&1; tail -1 gpurun_out/ev/bench_ref.json
+rm -f gpurun_out/ev/bench_grids.jsonl
+for gr in "300 300 90" "600 600 90"; do timeout 600 python bench.py --grid $gr --steps 40 --warmup 5 --no-cpu 2>/dev/null | tail -1 >> gpurun_out/ev/bench_grids.jsonl; done
+cat gpurun_out/ev/bench_grids.jsonl
 rm -f gpurun_out/ev/press.jsonl
 for path in 2 1 3; do timeout 300 python scripts/bench_press.py 150 150 90 --path $path >> gpurun_out/ev/press.jsonl; done
 for path in 1 3; do timeout 300 python scripts/bench_press.py 512 512 90 --path $path --reps 3 >> gpurun_out/ev/press.jsonl; done
