@@ -390,7 +390,7 @@ __global__ void k_divergence(Geo g, Spac s, const float* __restrict__ u, const f
 // fgh_old (interior: full chain; halo: adam only), and rhs (interior).
 // ---------------------------------------------------------------------------
 template <bool P2>
-__global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const float* __restrict__ vb,
+__global__ void __launch_bounds__(128) k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const float* __restrict__ vb,
                             const float* __restrict__ wb, const float* __restrict__ mask,
                             float* __restrict__ fgh, float* __restrict__ fgh_old, float* __restrict__ ua,
                             float* __restrict__ va, float* __restrict__ wa, float* __restrict__ rhs, float vn,
@@ -404,13 +404,17 @@ __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const f
     long long c = cidx(g, i, j, k);
     bool interior = i >= 1 && i <= g.im && j >= 1 && j <= g.jm && k >= 1 && k <= g.km;
     if (interior) {
+      // the last-used operands first: their DRAM latency overlaps velfg / les
+      const float m = mask[c];
+      float fo[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) fo[a] = fgh_old[3 * c + a];
       float f[3];
       f[0] = velfg_point<0, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       f[1] = velfg_point<1, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       f[2] = velfg_point<2, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       if (!(finite32(f[0]) && finite32(f[1]) && finite32(f[2]))) bits |= F_VELFG;
       // feedbf
-      const float m = mask[c];
       const float coef = (P2 && s.dtp2) ? m * s.rdt : m / dt;
       const float keep = 1.0f - m;
       const float vel[3] = {ub[c], vb[c], wb[c]};
@@ -436,7 +440,7 @@ __global__ void k_fused_rhs(Geo g, Spac s, const float* __restrict__ ub, const f
       float nf[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        nf[a] = 1.5f * f[a] - 0.5f * fgh_old[3 * c + a];
+        nf[a] = 1.5f * f[a] - 0.5f * fo[a];
       }
       if (!(finite32(nf[0]) && finite32(nf[1]) && finite32(nf[2]))) bits |= F_ADAM;
 #pragma unroll
