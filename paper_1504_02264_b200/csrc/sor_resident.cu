@@ -548,34 +548,18 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (tx && tid == 0) tx[6] = gtimer();
 
-  // tags: pass n of this launch is tag0 + n + 2 (the initial publish below
-  // plays passes -2 and -1); *epoch advances by the tags a launch uses, so
-  // tags never repeat across launches and stale words can never match
+  // tags: pass n of this launch is tag0 + n + 2; *epoch advances by the tags
+  // a launch uses, so tags never repeat across launches and stale words can
+  // never match.  No initial publish: pass 0 needs the neighbours' initial
+  // colour-1 faces and pass 1 (across an odd-jm wrap) their initial colour-0
+  // faces -- exactly the values the halo columns were just loaded with (from
+  // p, whose x-halo planes hold the neighbour slab's values), so those
+  // receives are skipped.
   const unsigned tag0 = 1u + *a.epoch;
-  // initial publish: both colours of the boundary columns, as passes -2
-  // (colour 0) and -1 (colour 1) of the ring of face buffers
-  for (int w = tid; w < nbnd * 2 * KK; w += nth) {
-    const int c = w / (2 * KK), r = w - c * 2 * KK;
-    const int col_c = r >= KK ? 1 : 0, sl = r - col_c * KK;
-    const int2 f = pubcol[c];
-    const float v = S[(coltab[c] & CB_MASK) + r];
-    unsigned long long* X = a.xbuf + (2 + col_c) * bstride + (long long)tile * tstride;
-    const unsigned tag = tag0 + (unsigned)col_c;
-    const unsigned long long word = ((unsigned long long)tag << 32) | __float_as_uint(v);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int o = h ? f.y : f.x;
-      if (o < 0) continue;
-      if (SLAB && (o & PUB_RW))
-        st_ll_sys(a.peer_w + (2 + col_c) * bstride + ghost_e + (o & PUB_OFF) + sl, word);
-      else if (SLAB && (o & PUB_RE))
-        st_ll_sys(a.peer_e + (2 + col_c) * bstride + ghost_w + (o & PUB_OFF) + sl, word);
-      else
-        st_ll_word(X + o + sl, word);
-    }
-  }
 
+  if (tx && tid == 0) tx[7] = gtimer();
   // runs: every thread gets about one boundary run and one interior run
   const int nint = ncol - nbnd;
   const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
@@ -625,6 +609,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     }
   }
   bool timed_out = false;
+  unsigned rwrapm = 0;  // slot-pair bits (2u, 2u + 1) of the wrap pairs
+#pragma unroll
+  for (int u = 0; u < RCVP; ++u)
+    if ((rwrap >> u) & 1u) rwrapm |= 3u << (2 * u);
   double acc = 0.0;
 
   unsigned long long* tr = a.trace ? a.trace + ((long long)tile * 2 * a.n_iter) * NST : nullptr;
@@ -635,7 +623,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     if (a.debug & 4) return;
     const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
     const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
-    const unsigned vm = (n & 1) ? rval1 : rval0;
+    const unsigned vm = ((n & 1) ? rval1 : rval0) & (n == 1 ? ~rwrapm : ~0u);
 #pragma unroll
     for (int u = 0; u < RCVP; ++u)
       if ((vm >> (2 * u)) & 3u) {
@@ -644,7 +632,6 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
         else ld_ll2(src, v[u][0], v[u][1]);
       }
   };
-  issue_receive(0);
   for (int n = 0; n < 2 * a.n_iter; ++n) {
     const int nrd = n & 1;
     if (tr && tid == 0) tr[NST * n + 0] = gtimer();
@@ -652,12 +639,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     // slots: pass n-1's publish, or pass n-2's across an odd-jm periodic wrap.
     // Those slots were last read in pass n-2, which every thread finished
     // before the barrier of pass n-1, so no barrier is needed before this.
-    if (!(a.debug & 4)) {
+    if (n > 0 && !(a.debug & 4)) {
       const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
       const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
       float* Sd = S + (1 - nrd) * KK;
-      const unsigned vm = nrd ? rval1 : rval0;
+      const unsigned vm = (nrd ? rval1 : rval0) & (n == 1 ? ~rwrapm : ~0u);
 #pragma unroll
       for (int u = 0; u < RCVP; ++u) {
         const bool w2 = (rwrap >> u) & 1u;
@@ -687,6 +674,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
         if (e.y < 0) continue;
         const int kps = (((1 - nrd) ^ (e.z & 1)) + e.w + 1) & 1;
         const bool w2 = e.z & 1;
+        if (w2 && n == 1) continue;  // initial values, already loaded
         const unsigned want = w2 ? t2 : t1;
         for (int h = 0; h < 2; ++h) {
           const int sl = sl0 + h;

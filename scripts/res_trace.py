@@ -40,9 +40,11 @@ print("per-tile work after receive (us): min %.2f median %.2f max %.2f" % (comp.
 ext = buf[nt * 100 * NST: nt * 100 * NST + nt * 8].reshape(nt, 8).astype(np.int64)
 if ext[:, 5].max() > 0:
     t00 = ext[:, 0].min()
-    e = (ext[:, :6] - t00) / 1e3
+    e = (ext[:, :8] - t00) / 1e3
     print("phases around the pass loop (us, mean over tiles): entry->loop %.2f  loop %.2f  write-back %.2f  "
           "grid sync %.2f  residuals %.2f  (kernel span %.2f)" % (
               (e[:, 1] - e[:, 0]).mean(), (e[:, 2] - e[:, 1]).mean(), (e[:, 3] - e[:, 2]).mean(),
               (e[:, 4] - e[:, 3]).mean(), (e[:, 5] - e[:, 4]).mean(), e[:, 5].max() - e[:, 0].min()))
-
+    print("prologue (us, mean over tiles): tables + loads %.2f  initial publish %.2f  receive setup %.2f  "
+          "(first tile entry -> last tile entry %.2f)" % ((e[:, 6] - e[:, 0]).mean(), (e[:, 7] - e[:, 6]).mean(),
+                                                         (e[:, 1] - e[:, 7]).mean(), e[:, 0].max() - e[:, 0].min()))
