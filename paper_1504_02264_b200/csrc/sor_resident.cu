@@ -141,6 +141,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 constexpr int ROW_PAD_MAX = 31;  // row padding of the column grid (chosen per tile shape by the plan)
+// Pair layout (RES_PAIRS): KK even, column stride CW = 4 KK + 2 and even row
+// pads, so every column base is 8-byte aligned and the boundary walk's slot
+// pairs move with 64-bit shared accesses (16 lanes on consecutive pairs of a
+// column: conflict free).  The interior runs stay scalar: the checkerboard's
+// alternating slot offset keeps their bank load at the odd-stride layout's
+// (the plan's row-pad model; measured: pair-wise runs diverge between the
+// two column parities and were slower).  RES_PAIRS=0: CW = 4 KK + 1.
+#ifndef RES_PAIRS
+#define RES_PAIRS 1
+#endif
+constexpr int CW_EXTRA = RES_PAIRS ? 2 : 1;
 
 __device__ __forceinline__ int tile_lo(int t, int n, int nt) { return 1 + (int)(((long long)t * n) / nt); }
 
@@ -284,6 +295,26 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
     if (v0 || v1) {
       const float* o = So + (cb + s0);  // other colour, same k as slot s0
       float* ce = Sc + (cb + s0);
+#if RES_PAIRS
+      // (8-byte aligned: cb, KK and s0 are even)
+      const float2 c2 = *reinterpret_cast<const float2*>(ce);
+      const float2 e2 = *reinterpret_cast<const float2*>(o + sI);
+      const float2 w2 = *reinterpret_cast<const float2*>(o - sI);
+      const float2 n2 = *reinterpret_cast<const float2*>(o + CW);
+      const float2 s2 = *reinterpret_cast<const float2*>(o - CW);
+      const float2 o2 = *reinterpret_cast<const float2*>(o);
+      const float ox = o[kp ? 2 : -1];
+      const float2 r2 = *reinterpret_cast<const float2*>(ce + 2 * KK);
+      const float pc0 = c2.x, pc1 = c2.y;
+      const float pE0 = e2.x, pE1 = e2.y;
+      float pW0 = w2.x, pW1 = w2.y;
+      const float pN0 = n2.x, pN1 = n2.y;
+      const float pS0 = s2.x, pS1 = s2.y;
+      float pB0 = kp ? o2.x : ox;        // k - 1 of the first cell
+      const float pTB = kp ? o2.y : o2.x;  // k + 1 of the first = k - 1 of the second
+      const float pT1 = kp ? ox : o2.y;
+      const float r0 = r2.x, r1 = r2.y;
+#else
       const float pc0 = ce[0], pc1 = ce[1];
       const float pE0 = o[sI], pE1 = o[sI + 1];
       float pW0 = o[-sI], pW1 = o[-sI + 1];
@@ -293,6 +324,7 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
       const float pTB = o[kp];           // k + 1 of the first = k - 1 of the second
       const float pT1 = o[kp + 1];
       const float r0 = ce[2 * KK], r1 = ce[2 * KK + 1];
+#endif
       float pB1 = pTB;
       if (PRESS) {
         if (ci & (1u << 29)) {  // physical west: p[0] -> p[1]
@@ -318,8 +350,12 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
       const float rel1 = a.om * (a.cn1 * (nb1 - r1) - pc1);
       const float np0 = v0 ? pc0 + rel0 : pc0;
       const float np1 = v1 ? pc1 + rel1 : pc1;
+#if RES_PAIRS
+      *reinterpret_cast<float2*>(ce) = make_float2(np0, np1);  // (an unused slot keeps its value)
+#else
       if (v0) ce[0] = np0;
       if (v1) ce[1] = np1;
+#endif
       const unsigned long long w0 = tagw | __float_as_uint(np0), w1 = tagw | __float_as_uint(np1);
       const int2 pub = pubcol[c];  // a column lies on at most two faces
 #pragma unroll
@@ -422,7 +458,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   const int TI = I1 - I0, TJ = J1 - J0;
   const int KK = pl.kk, KT = pl.kt, km = g.km;
   const int KKF = (KK + 1) & ~1;  // face-buffer words per column: even, so slot pairs are 16-byte aligned
-  const int CW = 4 * KK + 1;                 // floats per column (odd: lanes in different columns spread over banks)
+  const int CW = 4 * KK + CW_EXTRA;          // floats per column (see RES_PAIRS)
   // column stride along i, padded so that sI = (TJ - 2) CW (mod 32): the
   // interior columns then sit at CW * (ordinal) + const modulo the 32 banks,
   // and a warp's lanes on 32 consecutive interior columns never conflict
@@ -661,8 +697,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
             const unsigned long long* src = (w2 ? XB2 : XB1) + roff[u] + h;
             v[u][h] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
           }
-          Sd[rdst[u] + h] = __uint_as_float((unsigned)v[u][h]);
+          if (!RES_PAIRS) Sd[rdst[u] + h] = __uint_as_float((unsigned)v[u][h]);
         }
+        // pair layout: both slots in one 8-byte store (a slot without a
+        // published cell is a k halo slot of a halo column, never read)
+        if (RES_PAIRS && ((vm >> (2 * u)) & 3u))
+          *reinterpret_cast<float2*>(Sd + rdst[u]) =
+              make_float2(__uint_as_float((unsigned)v[u][0]), __uint_as_float((unsigned)v[u][1]));
       }
       // pairs beyond the register-held ones (large tiles / deep columns), one
       // word at a time
@@ -781,7 +822,7 @@ static int g_num_sms = -1;
 static int g_max_smem = -1;
 
 static size_t plan_smem(int tim, int tjm, int kk) {
-  const int cw = 4 * kk + 1;
+  const int cw = 4 * kk + CW_EXTRA;
   const size_t arrays = 4ull * ((((size_t)cw * (tjm + 2) + ROW_PAD_MAX) * (tim + 2) + 3) & ~(size_t)3);  // p and rhs, 2 colours each
   const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
   const size_t pubcol = 8ull * ((tim * tjm + 1) & ~1);
@@ -794,7 +835,7 @@ static size_t plan_smem(int tim, int tjm, int kk) {
 // column base + (1 - kp) (kp alternates with the column parity); the sum
 // over warps and both colours of the most-loaded bank.
 static int interior_bank_load(int TI, int TJ, int kk, int pad) {
-  const int cw = 4 * kk + 1, sI = (TJ + 2) * cw + pad;
+  const int cw = 4 * kk + CW_EXTRA, sI = (TJ + 2) * cw + pad;
   const int nj = TJ - 2, nint = (TI - 2) * nj;
   int load = 0;
   for (int nrd = 0; nrd < 2; ++nrd)
@@ -815,7 +856,7 @@ static int interior_bank_load(int TI, int TJ, int kk, int pad) {
 static int best_row_pad(int TI, int TJ, int kk) {
   if (TI <= 2 || TJ <= 2) return 0;
   int best = 0, bl = 1 << 30;
-  for (int pad = 0; pad <= ROW_PAD_MAX; ++pad) {
+  for (int pad = 0; pad <= ROW_PAD_MAX; pad += RES_PAIRS ? 2 : 1) {
     const int l = interior_bank_load(TI, TJ, kk, pad);
     if (l < bl) {
       bl = l;
@@ -851,6 +892,7 @@ static ResPlan plan_resident_uncached(const Geo& g, int device, int max_tiles) {
   if (g_num_sms <= 0) return pl;
   if (max_tiles <= 0 || max_tiles > g_num_sms) max_tiles = g_num_sms;
   pl.kk = ((g.km + 1) >> 1) + 1;
+  if (RES_PAIRS) pl.kk = (pl.kk + 1) & ~1;
   pl.kt = (g.km + 1) >> 1;
   size_t best = (size_t)-1;
   // tiles of at least 2 x 2 columns: a column then lies on at most two faces
