@@ -771,27 +771,42 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     // source is this column (les.py:341-355: k first, then j, then i)
     int ti_[2] = {i, (PRESS && i == 1 && g.west_bc) ? 0 : -1};  // (a slab's inner x halo is the neighbour's)
     int tj_[3] = {j, (PRESS && j == 1) ? g.jm + 1 : -1, (PRESS && j == g.jm) ? 0 : -1};
-    for (int k = lane; k <= km + 1; k += 32) {
-      const int kr = k == 0 ? 1 : (k > km ? km : k);
-      const float v = S[cb + colour(i + g.ioff, j, kr) * KK + (kr >> 1)];
-      const bool own = k >= 1 && k <= km;
-      if (own && !finite32(v)) bad = F_PRESS;
-      const float hv = (k == km + 1) ? 0.0f : v;
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        if (ti_[x] < 0) continue;
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-          if (tj_[y] < 0) continue;
-          const bool self = x == 0 && y == 0;
-          if (self && !own && !PRESS) continue;  // stored halo: untouched
-          a.p[cidx(g, ti_[x], tj_[y], k)] = self && own ? v : hv;
-        }
+    if (!(PRESS && ((i == 1 && g.west_bc) || j == 1 || j == g.jm || (i == g.im && g.east_bc)))) {
+      // (warp-uniform) no halo column takes its value from this one: the
+      // column itself, with the press k halo (p[0] = p[1], p[km+1] = 0)
+      float* dst = a.p + cidx(g, i, j, 0);
+      const int c0 = colour(i + g.ioff, j, 0);
+      for (int k = lane; k <= km + 1; k += 32) {
+        const int kr = k == 0 ? 1 : (k > km ? km : k);
+        const float v = S[cb + (c0 ^ (kr & 1)) * KK + (kr >> 1)];
+        const bool own = k >= 1 && k <= km;
+        if (own && !finite32(v)) bad = F_PRESS;
+        if (own) dst[k] = v;
+        else if (PRESS) dst[k] = (k == km + 1) ? 0.0f : v;
       }
-      if (PRESS && i == g.im && g.east_bc) {  // east face is Dirichlet 0 for every j' mapped here
+    } else {
+      for (int k = lane; k <= km + 1; k += 32) {
+        const int kr = k == 0 ? 1 : (k > km ? km : k);
+        const float v = S[cb + colour(i + g.ioff, j, kr) * KK + (kr >> 1)];
+        const bool own = k >= 1 && k <= km;
+        if (own && !finite32(v)) bad = F_PRESS;
+        const float hv = (k == km + 1) ? 0.0f : v;
 #pragma unroll
-        for (int y = 0; y < 3; ++y)
-          if (tj_[y] >= 0) a.p[cidx(g, g.im + 1, tj_[y], k)] = 0.0f;
+        for (int x = 0; x < 2; ++x) {
+          if (ti_[x] < 0) continue;
+#pragma unroll
+          for (int y = 0; y < 3; ++y) {
+            if (tj_[y] < 0) continue;
+            const bool self = x == 0 && y == 0;
+            if (self && !own && !PRESS) continue;  // stored halo: untouched
+            a.p[cidx(g, ti_[x], tj_[y], k)] = self && own ? v : hv;
+          }
+        }
+        if (PRESS && i == g.im && g.east_bc) {  // east face is Dirichlet 0 for every j' mapped here
+#pragma unroll
+          for (int y = 0; y < 3; ++y)
+            if (tj_[y] >= 0) a.p[cidx(g, g.im + 1, tj_[y], k)] = 0.0f;
+        }
       }
     }
   }
