@@ -286,7 +286,7 @@ def run_gpu(args):
     N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
     stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0) + 1  # + async bookkeeping kernel
+    kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0)  # asynchronous step, bookkeeping included
     sor_path = {1: "unfused colour passes", 2: "shared-memory-resident persistent kernel",
                 3: "colour-fused streaming iterations"}[
         lib.lesb_sor_path_in_use(hw.h, 0)]

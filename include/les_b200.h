@@ -143,8 +143,8 @@ int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profil
 int lesb_set_inflow(lesb_handle h, const float* in_u, const float* in_v, const float* in_w);
 int lesb_step_async(lesb_handle h, int n_iter, int scheme, float omega);
 int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_stage);
-/* Number of kernel launches one step enqueues (evidence for gpu_launches;
- * the asynchronous variant adds one bookkeeping kernel). */
+/* Number of kernel launches one asynchronous step (lesb_step_async)
+ * enqueues, its bookkeeping included (evidence for gpu_launches). */
 int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme);
 /* Device-to-device copy of the seven state fields between two domains of
  * the same shape on the same device (benchmark re-initialisation). */

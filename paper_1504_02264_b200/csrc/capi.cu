@@ -58,23 +58,10 @@ int fail(int code, const std::string& msg) {
 
 enum { MODE_SYNC = 0, MODE_ASYNC = 1 };
 
-// device-side step bookkeeping for asynchronous runs
-struct StepBook {
-  unsigned flags;       // stage bits of the current (or first failing) step
-  unsigned steps;       // steps enqueued and completed on the device
-  int fail_step;        // -1 while no step failed
-  unsigned fail_flags;  // stage bits of the first failing step
-  unsigned err;         // device-side solver error (neighbour wait timed out)
-};
-
+// device-side step bookkeeping for asynchronous runs: lesb::StepBook
+// (lesb_kernels.h); the resident solver does it itself when it ends the step
 __global__ void k_step_tail(StepBook* b) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    if (b->flags && b->fail_step < 0) {
-      b->fail_step = (int)b->steps;
-      b->fail_flags = b->flags;
-    }
-    b->steps += 1;
-  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) step_book_update(b);
 }
 
 int first_stage(unsigned bits) {
@@ -383,7 +370,8 @@ cudaError_t enqueue_press(lesb_domain* h, int n_iter, int scheme, float omega, b
 // The full step: velnw+bondv1 (A -> B), velfg+feedbf+les+adam+rhs (B -> A), press.
 // With timing on, event records are captured between the phases:
 // ev0 | velnw+bondv1 | ev1 | fused | ev2 | SOR passes | ev3 | halo + reduction | ev4
-cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omega) {
+cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omega, StepBook* tail_book = nullptr,
+                              bool* tail_done = nullptr) {
   unsigned* flags = &h->book_d->flags;
   auto mark = [&](int i) {
     if (h->timing) cudaEventRecordWithFlags(h->ev[i], h->st, cudaEventRecordExternal);
@@ -405,6 +393,10 @@ cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omeg
   SorMarks marks{h->timing ? h->ev[3] : nullptr};
   ResidentBufs rb = h->rbufs();
   const bool res_slab = h->link.comm && rb.use && scheme == 0;  // resident solver exchanging through peer memory
+  if (!h->link.comm) {  // the solve ends the step: it may take over the bookkeeping
+    rb.book = tail_book;
+    rb.book_used = tail_done;
+  }
   ExchangeHook hook{h->link.comm && !res_slab ? nccl_p_hook : nullptr, h};
   cudaError_t e = enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, 1, h->partials,
                               h->res_d, flags, h->st, &hook, &marks, &rb);
@@ -431,11 +423,13 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
     cudaMemsetAsync(&h->book_d->err, 0, sizeof(unsigned), h->st);
     cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * h->g.km * sizeof(float), cudaMemcpyHostToDevice, h->st);
   }
-  cudaError_t body_err = enqueue_step_body(h, n_iter, scheme, omega);
+  bool tail_done = false;
+  cudaError_t body_err =
+      enqueue_step_body(h, n_iter, scheme, omega, mode == MODE_ASYNC ? h->book_d : nullptr, &tail_done);
   if (mode == MODE_SYNC) {
     cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st);
     cudaMemcpyAsync(h->book_h, h->book_d, sizeof(StepBook), cudaMemcpyDeviceToHost, h->st);
-  } else {
+  } else if (!tail_done) {
     k_step_tail<<<1, 32, 0, h->st>>>(h->book_d);
   }
   cudaError_t e = cudaStreamEndCapture(h->st, &graph);
@@ -1010,7 +1004,10 @@ int lesb_last_step_times(lesb_handle h, float* ms) {
 int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
   if (!h) return fail(LESB_E_ARG, "null handle");
   const int path = lesb_sor_path_in_use(h, scheme);
-  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, path == 2, path == 3);
+  // + the asynchronous step's bookkeeping kernel, unless the resident solver
+  // ends the step and does it (single domain)
+  const int tail = (path == 2 && !h->link.comm) ? 0 : 1;
+  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, path == 2, path == 3) + tail;
 }
 
 // ---- solver on host buffers ----

@@ -22,6 +22,24 @@ struct SorMarks {
 
 // Buffers of the shared-memory-resident red-black solver (sor_resident.cu);
 // use == 0 forces the streaming kernels.
+// device-side step bookkeeping for asynchronous runs (capi.cu)
+struct StepBook {
+  unsigned flags;       // stage bits of the current (or first failing) step
+  unsigned steps;       // steps enqueued and completed on the device
+  int fail_step;        // -1 while no step failed
+  unsigned fail_flags;  // stage bits of the first failing step
+  unsigned err;         // device-side solver error (neighbour wait timed out)
+};
+
+// the end-of-step update (one thread, after every stage's flags are final)
+__device__ __forceinline__ void step_book_update(StepBook* b) {
+  if (b->flags && b->fail_step < 0) {
+    b->fail_step = (int)b->steps;
+    b->fail_flags = b->flags;
+  }
+  b->steps += 1;
+}
+
 struct ResidentBufs {
   int use;
   int device;
@@ -31,6 +49,10 @@ struct ResidentBufs {
   unsigned* err;
   void* peer_w = nullptr;  // x-slab: neighbour slabs' face buffers (peer memory)
   void* peer_e = nullptr;
+  // asynchronous step: the resident solver, the step's last kernel, also does
+  // the end-of-step bookkeeping (*book_used is set when it took it over)
+  StepBook* book = nullptr;
+  bool* book_used = nullptr;
 };
 
 // stages.cu
@@ -109,6 +131,7 @@ struct ResidentCall {
   void* peer_w;  // x-slab neighbours' face buffers (another GPU's, mapped), or nullptr
   void* peer_e;
   int max_tiles = 0;  // tiles of the plan (0: every SM); slabs sharing a device use num_SMs / n
+  StepBook* book = nullptr;  // single domain: end-of-step bookkeeping after the solve (ResidentBufs::book)
 };
 cudaError_t launch_sor_resident(const ResidentCall& c, cudaStream_t st);
 cudaError_t launch_sor_resident_group(int n, const ResidentCall* cs, cudaStream_t st);

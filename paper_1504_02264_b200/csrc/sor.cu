@@ -440,11 +440,14 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
                         const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res) {
   if (scheme == 0 && res && res->use && !(hook && hook->fn) && resident_supported(g, cf, res->device)) {
     // one launch: passes, press halo + its non-finite check, residuals
-    const ResidentCall call{&g,      res->device, p,          rhs,      &cf,      om,      n_iter,
-                            policy,  res->xbuf,   res->epoch, partials, res_dev,  flags,   res->err,
-                            res->peer_w, res->peer_e};
+    ResidentCall call{&g,      res->device, p,          rhs,      &cf,      om,      n_iter,
+                      policy,  res->xbuf,   res->epoch, partials, res_dev,  flags,   res->err,
+                      res->peer_w, res->peer_e};
+    const bool book = res->book && !res->peer_w && !res->peer_e;
+    if (book) call.book = res->book;
     cudaError_t e = launch_sor_resident(call, st);
     if (e != cudaSuccess) return e;
+    if (book && res->book_used) *res->book_used = true;
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
     return cudaGetLastError();
   }

@@ -97,6 +97,7 @@ struct ResArgs {
   unsigned* err;     // set when a neighbour wait times out
   int debug;         // timing experiments only (LESB_RES_DEBUG): 1 no waits, 2 no updates, 4 no receive
   unsigned long long* trace;  // LESB_RES_TRACE: [ntiles][2 n_iter][NST] %globaltimer stamps, or nullptr
+  StepBook* book;             // end-of-step bookkeeping after the grid barrier (single domain), or nullptr
 };
 
 // Face exchange in the "LL" style: every published value travels with the
@@ -817,7 +818,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   cg::this_grid().sync();
   if (tx && tid == 0) tx[4] = gtimer();
   // fresh tags for the next launch (a group's slabs share one epoch word)
-  if (tid == 0 && blockIdx.x == 0) *a.epoch += (unsigned)(2 * a.n_iter + 2);
+  if (tid == 0 && blockIdx.x == 0) {
+    *a.epoch += (unsigned)(2 * a.n_iter + 2);
+    // every stage's flags are final here (the tiles raised theirs before the barrier)
+    if (!SLAB && a.book) step_book_update(a.book);
+  }
   const int per_pass = ntiles * RES_WARPS;
   for (int it = tile; it < a.n_iter; it += ntiles) {
     const double* q = a.partials + (long long)it * per_pass;
@@ -1007,6 +1012,7 @@ static ResArgs make_args(const ResidentCall& c, const ResPlan& pl) {
   static const int dbg = getenv("LESB_RES_DEBUG") ? atoi(getenv("LESB_RES_DEBUG")) : 0;
   a.debug = dbg;
   a.trace = nullptr;
+  a.book = c.book;
   return a;
 }
 
