@@ -10,7 +10,8 @@
 //
 //   for pass n (colour nrd = n & 1):
 //     receive: the neighbours' pass n-1 faces (self-validating LL words, one
-//       16-byte load per slot pair) into this tile's halo columns; barrier
+//       16-byte load per slot pair, issued during pass n-1's interior runs)
+//       into this tile's halo columns; barrier
 //     update the colour-nrd cells of the tile's BOUNDARY columns, two slots
 //       per work unit, publishing each pair of new values with one 16-byte
 //       store into the tile's face slots (or, on an x-slab edge, straight
