@@ -305,7 +305,8 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
       const float2 n2 = *reinterpret_cast<const float2*>(o + CW);
       const float2 s2 = *reinterpret_cast<const float2*>(o - CW);
       const float2 o2 = *reinterpret_cast<const float2*>(o);
-      const float ox = o[kp ? 2 : -1];
+      // (kept inside the column's colour array: at the ends the value is unused)
+      const float ox = o[kp ? (s0 + 2 < KK ? 2 : 1) : (s0 > 0 ? -1 : 0)];
       const float2 r2 = *reinterpret_cast<const float2*>(ce + 2 * KK);
       const float pc0 = c2.x, pc1 = c2.y;
       const float pE0 = e2.x, pE1 = e2.y;
