@@ -27,6 +27,10 @@ CLI_FUNCS = ("les_main", "run_boundary_audit")  # cli.py:23 binds les_main at im
 # cli.main dispatches through the _RUNNERS table built at import (cli.py:323-328)
 CLI_RUNNERS = {"boundary-audit": "run_boundary_audit"}
 SOR_FUNCS = ("solve_pressure", "redblack_iteration", "twinned_sweep")
+# gmcf_mini/__init__.py re-exports les_main and the solver entry points
+# (``from gmcf_mini import solve_pressure`` binds the package attribute)
+PKG_LES_FUNCS = ("les_main",)
+PKG_SOR_FUNCS = SOR_FUNCS
 
 _saved: dict = {}
 
@@ -40,6 +44,12 @@ def install(les_module=None, sor_module=None) -> None:
     if les_module is None:
         try:
             mods.append((importlib.import_module("gmcf_mini.cli"), CLI_FUNCS, _les))
+        except ImportError:
+            pass
+        try:
+            pkg = importlib.import_module("gmcf_mini")
+            mods.append((pkg, PKG_LES_FUNCS, _les))
+            mods.append((pkg, PKG_SOR_FUNCS, _sor))
         except ImportError:
             pass
     for mod, names, impl in mods:

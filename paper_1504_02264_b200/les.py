@@ -193,22 +193,40 @@ for _n in _ALL:
 # ---------------------------------------------------------------------------
 # reference FlowState objects: upload, run, copy the written fields back
 # ---------------------------------------------------------------------------
-_compat: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+# The reference FlowState is a non-frozen @dataclass: __hash__ is None, so it
+# cannot key a WeakKeyDictionary.  The device twin is cached by id() and the
+# entry is evicted by a finalizer when the caller's object dies (the weak
+# reference also guards against a recycled id).
+_compat: dict = {}
+
+
+def _compat_lookup(state):
+    ent = _compat.get(id(state))
+    if ent is not None and ent[0]() is state:
+        return ent[1]
+    return None
+
+
+def _compat_store(state, ds):
+    key = id(state)
+    try:
+        ref = weakref.ref(state)
+    except TypeError:  # no weak references (e.g. __slots__): do not cache
+        return
+    _compat[key] = (ref, ds)
+    weakref.finalize(state, _compat.pop, key, None)
 
 
 def _resolve(state):
     """(device state, write-back target or None)."""
     if isinstance(state, FlowState):
         return state, None
-    ds = _compat.get(state)
+    ds = _compat_lookup(state)
     g = state.grid
     if ds is None or ds.grid is not g:
         ds = FlowState(state.u, state.v, state.w, state.fgh, state.fgh_old, state.p, state.mask, g,
                        state.dt, state.vn, state.cs)
-        try:
-            _compat[state] = ds
-        except TypeError:
-            pass
+        _compat_store(state, ds)
     for n in _ALL:
         ds._host[n] = getattr(state, n)
     ds._dev_newer.clear()

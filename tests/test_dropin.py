@@ -94,3 +94,28 @@ def test_install_rebinds_cli_runners(ref):
     assert cli._RUNNERS["boundary-audit"] is orig_runner
     assert cli.run_boundary_audit is orig_fn
     assert cli.les_main is orig_main
+
+
+def test_resolve_accepts_reference_flowstate(ref):
+    """ADVICE r1 (high): the reference FlowState is an unhashable dataclass;
+    the compat path caches its device twin by id and evicts it with the
+    caller's object (no compute: FlowState construction does not touch the
+    device)."""
+    les, sor = ref
+    import gc
+
+    from paper_1504_02264_b200 import les as L
+
+    st = les.FlowState.create(sor.Grid.uniform(4, 3, 2, 2.0), dt=0.5)
+    with pytest.raises(TypeError):
+        hash(st)
+    ds, target = L._resolve(st)
+    assert target is st and isinstance(ds, L.FlowState)
+    assert ds._host["u"] is st.u
+    ds2, t2 = L._resolve(st)
+    assert ds2 is ds  # cached: one device domain per caller state
+    key = id(st)
+    assert key in L._compat
+    del st, target, t2
+    gc.collect()
+    assert key not in L._compat
