@@ -20,11 +20,14 @@ Arms
                8-step window that uploads the initial state from pinned host
                memory, runs 8 steps (inflow H2D, stage flags + residual
                history D2H per step) and downloads the six fields.
-  reference    the reference algorithm on the host CPU: the numpy port in
-               oracle/ (the reference is pure Python/numpy; single-threaded
-               RB path, 1 core), a bounded sample of full-size steps.
+  reference    the reference on the host CPU: the unmodified gmcf_mini.les.step
+               from baseline/_ref (scripts/install_reference.sh; the numpy
+               port in oracle/ only when that is absent), a bounded sample
+               of full-size config-2 steps on 1 core (the reference's
+               red-black path is single-threaded numpy).
 
-Multi-GPU (torchrun, N > 1): x-slab decomposition -- each
+Multi-GPU (N > 1; `--gpus N` re-launches itself under torch.distributed.run
+when WORLD_SIZE is unset): x-slab decomposition -- each
 rank owns a 150x150x90 slab of a (150 N)x150x90 grid ("scaling": "weak"),
 halo planes move by NCCL send/recv inside the step's CUDA graph; value
 counts slab-steps over all ranks divided by the max-over-ranks time.
@@ -51,8 +54,8 @@ METRIC = "LES time steps/sec and MLUPS at 1/2/4/8 B200; % of HBM-bandwidth roofl
 IM, JM, KM = 150, 150, 90
 N_ITER = 50
 REINIT = 8
-B_STEP = 216 + 16 * N_ITER      # algorithmic bytes / interior cell / step
 B_ITER = 12                     # SOR RB iteration, cn1 a scalar: p read + p write + rhs read
+B_STEP = 216 + B_ITER * N_ITER  # algorithmic bytes / interior cell / step: 816 (SURVEY 8(d), cn1 scalarised)
 WORKLOAD = "config2: 150x150x90, h=2, dt=0.5, 3x3 buildings, log-law inflow, RB SOR 50 iters"
 
 
@@ -177,46 +180,113 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm and CPU baseline (oracle port of the reference)
+# CPU reference arm and CPU baseline: the unmodified reference (gmcf_mini,
+# installed under baseline/_ref by scripts/install_reference.sh) when it is
+# importable, else the numpy port in oracle/ (pinned bitwise to it)
 # ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def _reference_les():
+    """gmcf_mini.les from baseline/_ref (or None).  The reference's own
+    module-level step, never rebound here (install() is not called)."""
+    if os.path.isdir(os.path.join(REF_DIR, "gmcf_mini")) and REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import gmcf_mini.coupling as rc
+        import gmcf_mini.les as rl
+        import gmcf_mini.sor as rs
+    except ImportError:
+        return None
+    if rl.step.__module__ != "gmcf_mini.les":
+        raise RuntimeError("gmcf_mini.les.step is rebound (drop-in installed): not the reference")
+    return rl, rs, rc
+
+
 def cpu_sample(max_steps: int, budget_s: float):
-    """Time full-size oracle steps (the reference's numpy algorithm) on host
-    cores: returns (steps/s, steps timed, seconds)."""
+    """Time full-size config-2 steps of the reference on one host core:
+    returns (steps/s, steps timed, seconds, kind).  kind "reference" = the
+    unmodified gmcf_mini.les.step (les.py:393-416), "port" = oracle/."""
     import golden_inputs as gi
-    from oracle import les_oracle as O
 
     st = gi.config2_state(IM, JM, KM)
-    o = O.OState.zeros(IM, JM, KM)
-    for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask", "dx1", "dy1", "dzn"):
-        getattr(o, n)[...] = st[n]
-    inflow = gi.default_inflow(KM)
+    inflow = gi.default_inflow(KM)  # == driver.generate_profile at the CLI defaults (tests/golden_inputs.py)
+    ref = _reference_les()
+    if ref is not None:
+        rl, rs, rc = ref
+        flow = rl.FlowState.create(rs.Grid.uniform(IM, JM, KM, 2.0), dt=0.5, vn=0.8, cs=0.14)
+        flow.mask[...] = st["mask"]
+        prof = rc.WindProfile(*inflow)
+        kind = "reference"
+
+        def one():
+            rl.step(flow, prof, n_iter=N_ITER)
+    else:
+        from oracle import les_oracle as O
+
+        o = O.OState.zeros(IM, JM, KM)
+        for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask", "dx1", "dy1", "dzn"):
+            getattr(o, n)[...] = st[n]
+        kind = "port"
+
+        def one():
+            O.step(o, *inflow, n_iter=N_ITER)
     done = 0
     t0 = time.perf_counter()
     while done < max_steps:
-        O.step(o, *inflow, n_iter=N_ITER)
+        one()
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return done / dt, done, dt
+    return done / dt, done, dt, kind
+
+
+def cpu_desc(n, secs, kind):
+    what = ("the unmodified reference gmcf_mini.les.step (baseline/_ref)" if kind == "reference"
+            else "the numpy port oracle/les_oracle.py (reference not importable)")
+    return (f"{n} full {IM}x{JM}x{KM} RB50 config-2 steps of {what} in {secs:.1f}s, from a fresh state; "
+            f"1 thread (the reference's red-black path is single-threaded numpy)")
+
+
+def config_dict(world: int) -> dict:
+    """The workload -- identical in both arms."""
+    return {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack",
+            "global_grid": [IM * world, JM, KM],
+            "parallelism": (f"x-slabs over {world} GPUs, {IM}x{JM}x{KM} per GPU" if world > 1 else "1 GPU"),
+            "l2": "GPU arm: flushed before every timed step (256 MB device write, untimed)"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     for _ in range(min(args.warmup, 1)):
         cpu_sample(1, 0)
-    rate, n, secs = cpu_sample(max(1, args.steps), 90.0)
-    cores = 1
-    sample = f"{n} full {IM}x{JM}x{KM} RB50 steps of the numpy port (oracle/les_oracle.py), 1 thread"
+    rate, n, secs, kind = cpu_sample(max(1, args.steps), 90.0)
+    sample = cpu_desc(n, secs, kind)
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": world,
         "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1000.0 / rate, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack"},
+        "config": config_dict(world),
         "mlups": rate * IM * JM * KM / 1e6,
-        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": 1, "kind": kind, "sample": sample,
+                         **cpu_info()},
         "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -378,22 +448,20 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        rate, n, secs = cpu_sample(3, 20.0)
-        cpu = {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
-               "sample": f"{n} full 150x150x90 RB50 steps of the numpy port in {secs:.1f}s, 1 thread"}
+        rate, n, secs, kind = cpu_sample(3, 20.0)
+        cpu = {"value": rate, "unit": "steps/s", "cores": 1, "kind": kind, "sample": cpu_desc(n, secs, kind),
+               **cpu_info()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "grid": [IM, JM, KM], "n_iter": N_ITER, "scheme": "redblack",
-                       "l2": "flushed before every timed step (256 MB device write, untimed)",
-                       "reinit_every_steps": REINIT,
-                       "parallelism": (f"x-slabs over {world} GPUs, {IM}x{JM}x{KM} per GPU, NCCL halo planes"
-                                       if world > 1 else "1 GPU"),
+            "config": config_dict(world),
+            "method": {"reinit_every_steps": REINIT,
                        "timing": "CUDA events on the domain stream around each CUDA-graph step replay",
-                       "sor_kernel": sor_path},
+                       "sor_kernel": sor_path,
+                       "exchange": "NCCL halo planes inside the step graph" if world > 1 else None},
             "mlups": value * n_int / 1e6,
             "step_roofline": {"bytes_per_cell": B_STEP, "achieved_gbs": step_gbs, "peak_gbs": hbm,
                               "frac": step_gbs / hbm, "peak_kind": peak_kind},
@@ -495,6 +563,17 @@ def main():
                     f"RB SOR 50 iters")
     if args.warmup < 3 and args.impl == "cuda":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver launches it
+        # that way itself; a plain `python bench.py --gpus N` does the same)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

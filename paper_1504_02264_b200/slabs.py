@@ -199,7 +199,8 @@ class SlabDomain:
                      "lesb_step")
         # the reference raises after the first stage (in step order) that left a
         # non-finite value anywhere in the grid: the minimum over ranks
-        first = torch.tensor([stage.value if rc == N.LESB_NONFINITE else 99], dtype=torch.int64)
+        dev = "cuda" if self.dist.get_backend() == "nccl" else "cpu"
+        first = torch.tensor([stage.value if rc == N.LESB_NONFINITE else 99], dtype=torch.int64, device=dev)
         self.dist.all_reduce(first, op=self.dist.ReduceOp.MIN)
         if int(first.item()) < 99:
             raise NumericsError(N.STAGE_NAMES[int(first.item())], "device stage check (slabs)")
