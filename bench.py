@@ -357,8 +357,8 @@ def run_gpu(args):
     stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0)  # asynchronous step, bookkeeping included
-    sor_path = {1: "unfused colour passes", 2: "shared-memory-resident persistent kernel",
-                3: "colour-fused streaming iterations"}[
+    sor_path = {1: "streaming colour passes, colour-split layout", 2: "shared-memory-resident persistent kernel",
+                3: "streaming colour passes, natural layout"}[
         lib.lesb_sor_path_in_use(hw.h, 0)]
 
     def reinit():
@@ -425,7 +425,7 @@ def run_gpu(args):
     b_solve = B_ITER * n_int * N_ITER
     achieved = b_solve / (sor_ms * 1e-3) / 1e9
     step_gbs = B_STEP * n_int / (ms_per_step * 1e-3) / 1e9
-    sor_kernel = {2: "k_sor_resident", 3: "k_sor_rbfused", 1: "k_sor_rb"}[lib.lesb_sor_path_in_use(hw.h, 0)]
+    sor_kernel = {2: "k_sor_resident", 1: "k_sor_rbs", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(hw.h, 0)]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:

@@ -109,7 +109,8 @@ struct lesb_domain {
   float* scratch = nullptr;  // im*jm*km
   std::map<std::tuple<int, int, int, unsigned>, cudaGraphExec_t> graphs;
   bool timing = false;
-  int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 colour-fused streaming
+  int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 natural-layout passes
+  float* split = nullptr;  // colour-split p / rhs of the streaming red-black passes (4 * SplitGeo::n floats)
   void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
   unsigned* repoch = nullptr;  // resident solver tag epoch
   // x-slab on NCCL ranks: the neighbour ranks' face buffers mapped through
@@ -135,19 +136,23 @@ struct lesb_domain {
   }
   ResidentBufs rbufs() const {
     // auto: the resident solver where the grid fits the SMs' shared memory,
-    // else the unfused colour passes (fastest streaming option measured so
-    // far, profiles/r1_v3_summary.md); the colour-fused kernel on request
-    const bool whole = g.west_bc && g.east_bc && g.ioff == 0;  // one domain (not an x-slab)
-    const bool res = (sor_path == 0 || sor_path == 2) && xbuf != nullptr && (whole || peer_ready);
-    const bool fz = sor_path == 3;
-    ResidentBufs rb{res, device, fz ? 1 : 0, xbuf, repoch, &book_d->err};
-    if (res && !whole) {
+    // else the streaming colour passes on the colour-split layout (path 3:
+    // the same passes on the natural layout, also the fallback for
+    // non-uniform coefficients)
+    const bool res = resident_in_use();
+    ResidentBufs rb{res, device, sor_path == 3 ? 1 : 0, xbuf, repoch, &book_d->err};
+    rb.split = split;
+    if (res && !(g.west_bc && g.east_bc && g.ioff == 0)) {  // x-slab: faces through the neighbours' buffers
       rb.peer_w = peer_w;
       rb.peer_e = peer_e;
     }
     return rb;
   }
   long long n_int() const { return (long long)g.im * g.jm * g.km; }
+  bool resident_in_use() const {
+    const bool whole = g.west_bc && g.east_bc && g.ioff == 0;  // one domain (not an x-slab)
+    return (sor_path == 0 || sor_path == 2) && xbuf != nullptr && (whole || peer_ready);
+  }
 };
 
 namespace {
@@ -243,9 +248,8 @@ bool map_slab_peers(lesb_domain* h) {
 }
 
 int ensure_partials(lesb_domain* h, int n_iter) {
-  const int maxblk = std::max(std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)),
-                                        resident_partials(h->g, h->device)),
-                               std::max(sor_blocks_fused(h->g, h->device), sor_blocks_march(h->g, h->device)));
+  const int maxblk = std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)),
+                              std::max(resident_partials(h->g, h->device), sor_blocks_split(h->g)));
   long long need = (long long)n_iter * 2 * maxblk + reduce_scratch(maxblk, n_iter);
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
@@ -263,6 +267,11 @@ int ensure_partials(lesb_domain* h, int n_iter) {
   if (h->link.comm && h->xbuf && !h->peer_tried) {
     h->peer_tried = true;
     map_slab_peers(h);  // on failure the slab keeps the streaming colour passes
+  }
+  if (!h->split && h->sor_path != 3 && !h->resident_in_use() && split_supported(h->g, h->sorc())) {
+    const size_t sb = 4 * split_geo(h->g).n * sizeof(float);
+    CK(cudaMalloc(&h->split, sb));
+    CK(cudaMemset(h->split, 0, sb));
   }
   if (n_iter > h->res_cap) {
     if (h->res_d) cudaFree(h->res_d);
@@ -321,8 +330,8 @@ long long field_count(lesb_domain* h, int f) { return (f == LESB_FGH || f == LES
 // im+depth) takes the east neighbour's first `depth` planes.  Velocities use
 // depth 2 (velfg's shifted derivative at local i = im, les.py:100-110), the
 // pressure depth 1.
-ncclResult_t nccl_exchange(lesb_domain* h, float* f, int depth, cudaStream_t st) {
-  const size_t si = (size_t)h->g.si;
+ncclResult_t nccl_exchange(lesb_domain* h, float* f, int depth, cudaStream_t st, long long plane = 0) {
+  const size_t si = plane ? (size_t)plane : (size_t)h->g.si;
   const int r = h->link.rank;
   ncclResult_t e = ncclGroupStart();
   if (e != ncclSuccess) return e;
@@ -349,9 +358,25 @@ void local_exchange(lesb_domain* h, float* lesb_domain::*which, int depth, cudaS
                                     cudaMemcpyDeviceToDevice, st);
 }
 
-void nccl_p_hook(void* ctx, float* p) {
+void nccl_p_hook(void* ctx, float* p, long long plane) {
   lesb_domain* h = static_cast<lesb_domain*>(ctx);
-  nccl_exchange(h, p, 1, h->st);
+  nccl_exchange(h, p, 1, h->st, plane);
+}
+
+// in-process neighbours, one colour array of the split layout: planes 0 and
+// im+1 of colour c take the neighbours' last / first interior planes
+void local_exchange_split(lesb_domain* h, int c, cudaStream_t st) {
+  const SplitGeo sg = split_geo(h->g);
+  const size_t fb = sg.spi * sizeof(float);
+  float* f = h->split + c * sg.n;
+  if (h->link.west) {
+    const lesb_domain* w = h->link.west;
+    const SplitGeo sw = split_geo(w->g);
+    cudaMemcpyAsync(f, w->split + c * sw.n + (size_t)w->g.im * sw.spi, fb, cudaMemcpyDeviceToDevice, st);
+  }
+  if (h->link.east)
+    cudaMemcpyAsync(f + (size_t)(h->g.im + 1) * sg.spi, h->link.east->split + c * split_geo(h->link.east->g).n + sg.spi,
+                    fb, cudaMemcpyDeviceToDevice, st);
 }
 
 // Enqueue the press stage on the stream: rhs = div(u)/dt, SOR, final halo.
@@ -586,6 +611,7 @@ int lesb_destroy(lesb_handle h) {
   if (h->repoch) cudaFree(h->repoch);
   if (h->gxbuf) cudaFree(h->gxbuf);
   if (h->gepoch) cudaFree(h->gepoch);
+  if (h->split) cudaFree(h->split);
   if (h->res_d) cudaFree(h->res_d);
   if (h->book_d) cudaFree(h->book_d);
   if (h->res_h) cudaFreeHost(h->res_h);
@@ -974,10 +1000,12 @@ int lesb_set_default_sor_path(int path) {
 
 int lesb_sor_path_in_use(lesb_handle h, int scheme) {
   if (!h) return fail(LESB_E_ARG, "null handle");
-  if (scheme != LESB_REDBLACK || h->sor_path == 1 || !h->coeffs_set) return 1;
-  const bool res = (h->sor_path == 0 || h->sor_path == 2) && resident_supported(h->g, h->sorc(), h->device);
+  if (scheme != LESB_REDBLACK || !h->coeffs_set) return 1;  // twinned: streaming sweeps
+  const bool whole = h->g.west_bc && h->g.east_bc && h->g.ioff == 0;
+  const bool res = (h->sor_path == 0 || h->sor_path == 2) && resident_supported(h->g, h->sorc(), h->device) &&
+                   (whole || h->peer_ready);
   if (res) return 2;
-  if (h->sor_path == 3 && fused_supported(h->g, h->sorc(), h->device)) return 3;
+  if (h->sor_path == 3 || !split_supported(h->g, h->sorc())) return 3;
   return 1;
 }
 
@@ -1007,7 +1035,7 @@ int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
   // + the asynchronous step's bookkeeping kernel, unless the resident solver
   // ends the step and does it (single domain)
   const int tail = (path == 2 && !h->link.comm) ? 0 : 1;
-  return 2 + sor_kernels_per_solve(h->g, n_iter, scheme, 1, path == 2, path == 3) + tail;
+  return 2 + sor_kernels_per_solve(h->g, h->sorc(), n_iter, scheme, 1, path == 2, path == 3) + tail;
 }
 
 // ---- solver on host buffers ----
@@ -1267,30 +1295,45 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
       cudaEventDestroy(ev_in);
     }
   }
+  // streaming passes: the colour-split layout where every slab supports it
+  bool split = !group_res && scheme == LESB_REDBLACK && h0->sor_path != 3;
+  for (int s = 0; s < n && split; ++s) split = hs[s]->split && split_supported(hs[s]->g, hs[s]->sorc());
+  if (split)
+    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, st);
   for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {
       for (int s = 0; s < n; ++s) {
         lesb_domain* h = hs[s];
-        const int nblk = scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g);
+        const int nblk = split ? sor_blocks_split(h->g)
+                               : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g));
         double* part = h->partials + ((long long)it * 2 + nrd) * nblk;
-        if (scheme == LESB_REDBLACK) {
+        if (split) {
+          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, 1, part, st);
+        } else if (scheme == LESB_REDBLACK) {
           launch_rb_pass(h->g, h->p, h->rhs, h->sorc(), omega, nrd, 1, part, st);
         } else {
           launch_tw_sweep(h->g, nrd == 0 ? h->p : h->pb, nrd == 0 ? h->pb : h->p, h->rhs, h->sorc(), omega, 1,
                           part, st);
         }
       }
-      for (int s = 0; s < n; ++s)
-        local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
+      for (int s = 0; s < n; ++s) {
+        if (split) local_exchange_split(hs[s], nrd, st);
+        else local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
+      }
     }
   }
-  for (int s = 0; s < n; ++s) launch_press_halo(hs[s]->g, hs[s]->p, &hs[s]->book_d->flags, st);
+  for (int s = 0; s < n; ++s) {
+    if (split) launch_split_unpack(hs[s]->g, hs[s]->split, hs[s]->p, 1, &hs[s]->book_d->flags, st);
+    else launch_press_halo(hs[s]->g, hs[s]->p, &hs[s]->book_d->flags, st);
+  }
   for (int s = 0; s < n; ++s) local_exchange(hs[s], &lesb_domain::p, 1, st);
   for (int s = 0; s < n; ++s) {
     lesb_domain* h = hs[s];
     if (!group_res)  // (the resident solver reduces its residuals itself)
-      launch_reduce_res(h->partials, scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g), n_iter,
-                        h->res_d, st);
+      launch_reduce_res(h->partials,
+                        split ? sor_blocks_split(h->g)
+                              : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g)),
+                        n_iter, h->res_d, st);
     CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   }

@@ -10,9 +10,20 @@ namespace lesb {
 // Called after every SOR pass / sweep and after the final halo
 // materialisation with the freshly written pressure buffer (x-slab halo
 // exchange for multi-GPU runs; unused on one GPU).
+// plane: floats per x plane of the buffer (natural p: Geo::si; one colour
+// array of the split layout: SplitGeo::spi).
 struct ExchangeHook {
-  void (*fn)(void* ctx, float* p);
+  void (*fn)(void* ctx, float* p, long long plane);
   void* ctx;
+};
+
+// Colour-split layout of p / rhs for the streaming red-black solver
+// (sor_split.cu): per colour (im+2) x (jm+2) rows of khp slots.
+struct SplitGeo {
+  int khp;        // slots per row: ceil((km+2)/2) rounded up to a multiple of 4
+  int kh4;        // khp / 4
+  long long spi;  // floats per x plane of one colour array: (jm+2) * khp
+  long long n;    // floats per colour array: (im+2) * spi
 };
 
 // Optional event recorded after the last SOR pass (stage timing).
@@ -43,7 +54,7 @@ __device__ __forceinline__ void step_book_update(StepBook* b) {
 struct ResidentBufs {
   int use;
   int device;
-  int fused;         // use the colour-fused streaming kernel (when the resident one is not used)
+  int natural;       // streaming passes on the natural layout (k_sor_rb) instead of the split one
   void* xbuf;        // resident_xbuf_words() 64-bit words, zero-initialised
   unsigned* epoch;   // one word, zero-initialised
   unsigned* err;
@@ -53,6 +64,7 @@ struct ResidentBufs {
   // the end-of-step bookkeeping (*book_used is set when it took it over)
   StepBook* book = nullptr;
   bool* book_used = nullptr;
+  float* split = nullptr;  // 4 * SplitGeo::n floats: p (colour 0, 1), rhs (colour 0, 1)
 };
 
 // stages.cu
@@ -90,22 +102,20 @@ void launch_press_halo(const Geo& g, float* p, unsigned* flags, cudaStream_t st)
 void launch_press_halo_copy(const Geo& g, const float* src, float* dst, unsigned* flags, cudaStream_t st);
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st);
 int reduce_scratch(int nblk, int n_iter);  // extra doubles launch_reduce_res needs after the partials
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused);
+int sor_kernels_per_solve(const Geo& g, const SorC& cf, int n_iter, int scheme, int policy, bool resident,
+                          bool natural);
 cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
                         int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
                         const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res = nullptr);
 
-// sor_fused.cu
-bool fused_supported(const Geo& g, const SorC& cf, int device);
-int sor_blocks_fused(const Geo& g, int device);
-cudaError_t launch_rb_fused(const Geo& g, int device, const float* pa, float* pb, const float* rhs, const SorC& cf,
-                            float om, int policy, double* partials, cudaStream_t st);
-
-// sor_march.cu
-bool march_supported(const Geo& g, const SorC& cf, int device);
-int sor_blocks_march(const Geo& g, int device);
-cudaError_t launch_rb_march(const Geo& g, int device, const float* pa, float* pb, const float* rhs, const SorC& cf,
-                            float om, int policy, double* partials, cudaStream_t st);
+// sor_split.cu
+SplitGeo split_geo(const Geo& g);
+bool split_supported(const Geo& g, const SorC& cf);
+int sor_blocks_split(const Geo& g);
+void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, cudaStream_t st);
+void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
+                     cudaStream_t st);
+void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st);
 
 // sor_resident.cu
 // max_tiles: 0 for every SM (one domain or one slab per GPU); num_SMs / n for

@@ -425,12 +425,16 @@ void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out
   k_reduce_res<<<n_iter, 256, 0, st>>>(scratch, nch, out);
 }
 
-int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool resident, bool fused) {
+int sor_kernels_per_solve(const Geo& g, const SorC& cf, int n_iter, int scheme, int policy, bool resident,
+                          bool natural) {
   if (resident && scheme == 0) return 1;
-  if (fused && scheme == 0) return n_iter + (policy == 1 || (n_iter & 1) ? 1 : 0) + 1;
+  const bool oddy = policy == 1 && (g.jm & 1);
+  const int red = (int)(reduce_scratch(scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g), n_iter) > 0) + 1;
+  if (scheme == 0 && !natural && split_supported(g, cf))  // pack, passes (+ y snapshots), unpack, reduction
+    return 1 + (oddy ? 4 : 2) * n_iter + 1 + ((int)(reduce_scratch(sor_blocks_split(g), n_iter) > 0) + 1);
   int per_iter = 2;
-  if (scheme == 0 && policy == 1 && (g.jm & 1)) per_iter = 4;
-  return per_iter * n_iter + (policy == 1 ? 1 : 0) + 1;
+  if (scheme == 0 && oddy) per_iter = 4;
+  return per_iter * n_iter + (policy == 1 ? 1 : 0) + red;
 }
 
 // Enqueue a full solve on p (in place).  TWINNED needs pb initialised to a
@@ -438,7 +442,8 @@ int sor_kernels_per_solve(const Geo& g, int n_iter, int scheme, int policy, bool
 cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, const SorC& cf, float om, int n_iter,
                         int scheme, int policy, double* partials, double* res_dev, unsigned* flags, cudaStream_t st,
                         const ExchangeHook* hook, const SorMarks* marks, const ResidentBufs* res) {
-  if (scheme == 0 && res && res->use && !(hook && hook->fn) && resident_supported(g, cf, res->device)) {
+  const bool hooked = hook && hook->fn;
+  if (scheme == 0 && res && res->use && !hooked && resident_supported(g, cf, res->device)) {
     // one launch: passes, press halo + its non-finite check, residuals
     ResidentCall call{&g,      res->device, p,          rhs,      &cf,      om,      n_iter,
                       policy,  res->xbuf,   res->epoch, partials, res_dev,  flags,   res->err,
@@ -451,29 +456,23 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
     return cudaGetLastError();
   }
-  if (scheme == 0 && res && res->fused && !(hook && hook->fn) && fused_supported(g, cf, res->device)) {
-    // colour-fused out-of-place iterations, ping-pong p <-> pb: the i-marching
-    // kernel, or the tile kernel where the marching one does not fit
-    // the marching kernel is experimental (slower than the tile kernel on
-    // B200 so far, profiles/r1_v3_summary.md): opt in with LESB_SOR_MARCH=1
-    const bool march = march_supported(g, cf, res->device) && getenv("LESB_SOR_MARCH") &&
-                       std::atoi(getenv("LESB_SOR_MARCH")) != 0;
-    const int nb = march ? sor_blocks_march(g, res->device) : sor_blocks_fused(g, res->device);
-    const size_t bytes = (size_t)(g.im + 2) * g.si * sizeof(float);
-    cudaError_t e = cudaMemcpyAsync(pb, p, bytes, cudaMemcpyDeviceToDevice, st);  // pb's halo = stored halo
-    if (e != cudaSuccess) return e;
+  if (scheme == 0 && res && res->split && !res->natural && split_supported(g, cf)) {
+    // colour-split streaming passes: split p and rhs, 2 n_iter unit-stride
+    // passes (each followed by the slab's plane exchange of the colour it
+    // wrote), merge back with the final halo_fn and the press check
+    const SplitGeo sg = split_geo(g);
+    const int nblk = sor_blocks_split(g);
+    launch_split_pack(g, p, rhs, res->split, st);
     for (int it = 0; it < n_iter; ++it) {
-      const float* src = (it & 1) ? pb : p;
-      float* dst = (it & 1) ? p : pb;
-      e = march ? launch_rb_march(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st)
-                : launch_rb_fused(g, res->device, src, dst, rhs, cf, om, policy, partials + (long long)it * 2 * nb, st);
-      if (e != cudaSuccess) return e;
+      for (int c = 0; c < 2; ++c) {
+        launch_rbs_pass(g, res->split, cf, om, c, policy, partials + ((long long)it * 2 + c) * nblk, st);
+        if (hooked) hook->fn(hook->ctx, res->split + c * sg.n, sg.spi);
+      }
     }
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
-    float* fin = (n_iter & 1) ? pb : p;
-    if (policy == 1) launch_press_halo_copy(g, fin, p, flags, st);
-    else if (fin != p) cudaMemcpyAsync(p, fin, bytes, cudaMemcpyDeviceToDevice, st);
-    launch_reduce_res(partials, nb, n_iter, res_dev, st);
+    launch_split_unpack(g, res->split, p, policy, policy == 1 ? flags : nullptr, st);
+    if (policy == 1 && hooked) hook->fn(hook->ctx, p, g.si);
+    launch_reduce_res(partials, nblk, n_iter, res_dev, st);
     return cudaGetLastError();
   }
   const int nblk = scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g);
@@ -482,19 +481,19 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
       double* part = partials + ((long long)it * 2 + nrd) * nblk;
       if (scheme == 0) {
         launch_rb_pass(g, p, rhs, cf, om, nrd, policy, part, st);
-        if (hook && hook->fn) hook->fn(hook->ctx, p);
+        if (hooked) hook->fn(hook->ctx, p, g.si);
       } else {
         const float* s = nrd == 0 ? p : pb;
         float* d = nrd == 0 ? pb : p;
         launch_tw_sweep(g, s, d, rhs, cf, om, policy, part, st);
-        if (hook && hook->fn) hook->fn(hook->ctx, d);
+        if (hooked) hook->fn(hook->ctx, d, g.si);
       }
     }
   }
   if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
   if (policy == 1) {
     launch_press_halo(g, p, flags, st);
-    if (hook && hook->fn) hook->fn(hook->ctx, p);
+    if (hooked) hook->fn(hook->ctx, p, g.si);
   }
   launch_reduce_res(partials, nblk, n_iter, res_dev, st);
   return cudaGetLastError();

@@ -25,8 +25,8 @@ SOR_AUTO, SOR_PASSES, SOR_RESIDENT, SOR_FUSED = 0, 1, 2, 3
 
 def set_sor_path(path: int) -> None:
     """Red-black solver implementation for new domains and the host-buffer
-    solver: 0 auto, 1 unfused colour passes, 2 shared-memory resident,
-    3 colour-fused streaming.  Results are bitwise identical; this only
+    solver: 0 auto, 1 streaming colour passes (colour-split layout), 2
+    shared-memory resident, 3 streaming colour passes on the natural layout.  Results are bitwise identical; this only
     selects the kernels."""
     from . import _native as N
 

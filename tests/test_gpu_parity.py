@@ -21,12 +21,13 @@ FIELDS = ("u", "v", "w", "fgh", "fgh_old", "p")
 RTOL_RES = 1e-12
 
 
-@pytest.fixture(scope="module", params=[1, 0, 3], ids=["passes", "resident", "fused"])
+@pytest.fixture(scope="module", params=[1, 0, 3], ids=["split", "resident", "natural"])
 def P(request):
-    """The package with the red-black solver forced to the unfused colour
-    passes (1), left on auto, which selects the shared-memory-resident
-    persistent kernel wherever the grid fits (0), or forced to the
-    colour-fused streaming kernel (3).  Every test runs on all three."""
+    """The package with the red-black solver forced to the streaming colour
+    passes on the colour-split layout (1), left on auto, which selects the
+    shared-memory-resident persistent kernel wherever the grid fits (0), or
+    forced to the streaming passes on the natural layout (3).  Every test
+    runs on all three."""
     import paper_1504_02264_b200 as pkg
 
     pkg.runtime.set_sor_path(request.param)
