@@ -1299,7 +1299,7 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
   bool split = !group_res && scheme == LESB_REDBLACK && h0->sor_path != 3;
   for (int s = 0; s < n && split; ++s) split = hs[s]->split && split_supported(hs[s]->g, hs[s]->sorc());
   if (split)
-    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, st);
+    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, 1, st);
   for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {
       for (int s = 0; s < n; ++s) {

@@ -112,7 +112,7 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
 SplitGeo split_geo(const Geo& g);
 bool split_supported(const Geo& g, const SorC& cf);
 int sor_blocks_split(const Geo& g);
-void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, cudaStream_t st);
+void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st);
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
                      cudaStream_t st);
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st);

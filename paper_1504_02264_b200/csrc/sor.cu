@@ -462,7 +462,7 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
     // wrote), merge back with the final halo_fn and the press check
     const SplitGeo sg = split_geo(g);
     const int nblk = sor_blocks_split(g);
-    launch_split_pack(g, p, rhs, res->split, st);
+    launch_split_pack(g, p, rhs, res->split, policy, st);
     for (int it = 0; it < n_iter; ++it) {
       for (int c = 0; c < 2; ++c) {
         launch_rbs_pass(g, res->split, cf, om, c, policy, partials + ((long long)it * 2 + c) * nblk, st);

@@ -13,19 +13,47 @@
 //   E/W/N/S: rows (i+-1, j) / (i, j+-1), the same slot t;
 //   T/B:     the same row, slots t + s and t + s - 1.
 // A colour pass therefore reads the other array, its own cells and the
-// colour's rhs, and writes its own cells, all unit-stride: a thread takes
-// four consecutive slots (one 16-byte access per array and neighbour row,
-// plus one scalar for the T/B shift), a warp 512 contiguous bytes.  The
-// natural layout's pass strides over both colours (every 32-byte sector it
-// touches is half the other colour), which is what kept the unfused pass at
-// ~20 B/cell/iteration of DRAM traffic instead of 16.
+// colour's rhs, and writes its own cells, all unit-stride.  The natural
+// layout's pass strides over both colours (every sector it touches is half
+// the other colour), which kept it at ~20 B/cell/iteration of DRAM traffic
+// instead of 16.
 //
-// p and rhs are split once per solve (k_split_pack) and p is merged back
-// once at the end (k_split_unpack), which also applies the final halo_fn of
-// the press policy in closed form and the press stage's non-finite check.
-// Arithmetic: sor_point's expression and order (A8), bitwise equal to the
-// other solvers; the residual is summed per thread in slot order, per block
-// by a fixed shuffle tree, and per iteration by launch_reduce_res.
+// Pass kernel.  A thread owns four consecutive slots (16-byte accesses) of
+// RBS_R consecutive rows j of one plane i and issues all their loads before
+// computing: its own cells, rhs, the other colour's rows (i+-1, j) and one
+// scalar for the T/B shift per row, and the other colour's rows j0-1 ..
+// j0+RBS_R of plane i once (row j's N is row j+1's centre row) -- for two
+// rows, twelve 16-byte loads and two 4-byte loads for eight cells, all in
+// flight together.  RBS_R is even, so the parity s of a thread's first row
+// is uniform per block (it depends on c and the plane) and the T/B
+// selection is compiled per parity.
+//
+// Halo policy.  STORED (halo_fn=None): the halos are p0's, read as stored.
+// PRESS (les._pressure_halo before every pass): the pack writes the
+// closed-form halo, and the pass keeps every halo cell a
+// stencil reads equal to its current source by mirror writes, so the pass
+// itself reads every neighbour plainly:
+//   W  p[0,j,k]    = p[1,j,k]   the cell itself: stored with it (other array, plane 0)
+//   B  p[i,j,0]    = p[i,j,1]   the cell itself: stored with it (other array, slot 0)
+//   E  p[im+1,j,k] = 0, T p[i,j,km+1] = 0: written by the pack, never changed
+//   S/N (even jm)  p[i,0,k] = p[i,jm,k], p[i,jm+1,k] = p[i,1,k]: rows jm / 1
+//                  are the same colour as rows 0 / jm+1 and are mirrored
+//                  into them when written; their readers run in the next pass
+//   S/N (odd jm)   the halo rows and their sources share the pass: a
+//                  pre-pass snapshot (k_split_refresh_y), as the reference's
+//                  halo_fn before the pass
+// Each mirrored slot is read in the pass only by the thread that writes it,
+// before it writes it.  k_split_unpack merges p back with the final halo_fn
+// in closed form and the press stage's non-finite check.
+//
+// Arithmetic: A8 in the reference's order, bitwise equal to the other
+// solvers; the residual of a cell is fma((f64)rel, (f64)rel, acc) -- the
+// f64 product of two f32 values is exact, so this is the reference's
+// sum += rel*rel term -- summed per thread in row/slot order, per block by a
+// fixed shuffle tree, per iteration by launch_reduce_res.
+#include <algorithm>
+#include <cstdlib>
+
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
 
@@ -48,16 +76,28 @@ bool split_supported(const Geo& g, const SorC& cf) {
 
 namespace {
 
-constexpr int RBS_NT = 256;  // threads per pass block (x: float4 groups of a row, y: rows)
-constexpr int RBS_R = 2;     // rows per thread (j, j + blockDim.y)
+// build-time switches (scripts/build_variant.sh -D...): rows per thread,
+// minimum resident blocks
+#ifndef RBS_ROWS
+#define RBS_ROWS 2
+#endif
+#ifndef RBS_MINB
+#define RBS_MINB 1
+#endif
+constexpr int RBS_NT = 256;        // threads per pass block (x: float4 groups of a row, y: row runs)
+constexpr int RBS_R = RBS_ROWS;    // consecutive rows per thread (even: uniform first-row parity)
 
 inline void rbs_shape(const SplitGeo& s, int* bx, int* by) {
-  *bx = s.kh4 < 32 ? s.kh4 : 32;
+  *bx = s.kh4 < RBS_NT ? s.kh4 : RBS_NT;
   *by = RBS_NT / *bx;
   if (*by < 1) *by = 1;
 }
 
-// Split p and rhs: a warp per natural row (i, j), lanes over k.
+// Split p and rhs: a warp per natural row (i, j), lanes over k.  PRESS:
+// halo cells (not on a neighbour slab's plane) take the closed-form
+// halo_fn value (k: 0 -> 1, km+1 -> 0; then j periodic; then i: 0 -> 1,
+// im+1 -> 0) -- the state the reference's halo_fn leaves before pass 0.
+template <int POL>
 __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const float* __restrict__ p,
                                                     const float* __restrict__ rhs, float* __restrict__ ps,
                                                     float* __restrict__ rs) {
@@ -67,129 +107,343 @@ __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const fl
   const int lane = threadIdx.x & 31;
   const int i = (int)(row / (g.jm + 2)), j = (int)(row - (long long)i * (g.jm + 2));
   const int par = (i + g.ioff + j + 1) & 1;
-  const float* src_p = p + row * (g.km + 2);
+  const bool rowhalo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1;
+  const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+  const bool remap = POL == 1 && !foreign;
+  const bool zero_row = remap && i == g.im + 1;
+  const int ii = (remap && i == 0) ? 1 : i;
+  const int jj = (remap && rowhalo) ? (j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j)) : j;
+  const float* src_p = p + ((long long)ii * (g.jm + 2) + jj) * (g.km + 2);
   const float* src_r = rhs + row * (g.km + 2);
   const long long rb = row * sg.khp;
   for (int k = lane; k < g.km + 2; k += 32) {
+    float val;
+    if (zero_row || (remap && k == g.km + 1)) val = 0.0f;
+    else val = src_p[(remap && k == 0) ? 1 : k];
     const int c = (par + k) & 1;
     const long long d = c * sg.n + rb + (k >> 1);
-    ps[d] = src_p[k];
+    ps[d] = val;
     rs[d] = src_r[k];
   }
 }
 
-// One colour pass (colour c) in place on the split arrays.  POL 0: stored
-// halo; POL 1: press remaps (the W/B sources are the updated cell itself,
-// read before it is written; the S/N sources have the other colour for even
-// jm, and for odd jm the y halo rows hold a pre-pass snapshot, y_stored).
-template <int POL>
-__global__ void __launch_bounds__(RBS_NT) k_sor_rbs(Geo g, SplitGeo sg, float* __restrict__ ps,
-                                                    const float* __restrict__ rs, SorC cf, float om, int c,
-                                                    int y_stored, double* __restrict__ partials) {
-  __shared__ double red[RBS_NT / 32];
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // float4 group of the row
-  const int i = blockIdx.z + 1;
-  const int ig = i + g.ioff;
-  float* own = ps + (long long)c * sg.n;
-  const float* oth = ps + (long long)(c ^ 1) * sg.n;
-  const float* rc = rs + (long long)c * sg.n;
+// Pass loads go through the read-only (non-coherent) path: within a pass the
+// only locations written besides the thread's own cells are the PRESS
+// mirror slots, each read earlier in the pass by the thread that writes it.
+__device__ __forceinline__ float4 ld4(const float* a) { return __ldg(reinterpret_cast<const float4*>(a)); }
+__device__ __forceinline__ float ld1(const float* a) { return __ldg(a); }
+__device__ __forceinline__ void st4(float* a, float x, float y, float z, float w) {
+  *reinterpret_cast<float4*>(a) = make_float4(x, y, z, w);
+}
+
+// One row of four cells: S is the row parity (compile time).  nb/rel in
+// the reference's order (sor.py:164-171, 197).
+template <int S>
+__device__ __forceinline__ void rbs_row(const SorC& cf, float om, const float4& C, const float4& RH, const float4& E,
+                                        const float4& W, const float4& N, const float4& So, const float4& M,
+                                        float extra, const bool (&in)[4], float (&val)[4], double& acc) {
+  const float cv[4] = {C.x, C.y, C.z, C.w};
+  const float rv[4] = {RH.x, RH.y, RH.z, RH.w};
+  const float ev[4] = {E.x, E.y, E.z, E.w};
+  const float wv[4] = {W.x, W.y, W.z, W.w};
+  const float nv[4] = {N.x, N.y, N.z, N.w};
+  const float sv[4] = {So.x, So.y, So.z, So.w};
+  // T/B: S = 0 -> T = m[t], B = m[t-1] (t0-1: extra); S = 1 -> T = m[t+1] (t0+4: extra), B = m[t]
+  const float mv[6] = {S == 0 ? extra : M.x, M.x, M.y, M.z, M.w, S == 1 ? extra : M.w};
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const float pT = S == 0 ? mv[m + 1] : mv[m + 2];
+    const float pB = S == 0 ? mv[m] : mv[m + 1];
+    float nb = cf.w2l * ev[m];
+    nb = nb + cf.w2s * wv[m];
+    nb = nb + cf.w3l * nv[m];
+    nb = nb + cf.w3s * sv[m];
+    nb = nb + cf.w4l * pT;
+    nb = nb + cf.w4s * pB;
+    const float rel = om * (cf.cn1s * (nb - rv[m]) - cv[m]);
+    // non-interior slots (k halo, row padding) keep their stored value
+    val[m] = in[m] ? cv[m] + rel : cv[m];
+    const double d = in[m] ? (double)rel : 0.0;
+    acc = __fma_rn(d, d, acc);
+  }
+}
+
+// The rows of one thread: RBS_R consecutive rows from j0 (S0 = parity of
+// row j0), four slots each, marching along j with the other colour's rows
+// j-1, j, j+1 in registers.
+template <int POL, int S0>
+__device__ __forceinline__ void rbs_march(const Geo& g, const SplitGeo& sg, float* own, float* oth, const float* rh,
+                                          const SorC& cf, float om, int q, int i, int j0, double& acc) {
   const int spi = (int)sg.spi, khp = sg.khp;
-  const bool wfix = POL == 1 && i == 1 && g.west_bc;   // W -> the cell itself
-  const bool efix = POL == 1 && i == g.im && g.east_bc;  // E -> 0
+  // cells m of a parity-s row are interior iff 1 <= 8q + s + 2m <= km
+  bool in0[4], in1[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int k0 = 8 * q + 2 * m;
+    in0[m] = k0 >= 1 && k0 <= g.km;
+    in1[m] = k0 + 1 <= g.km;
+  }
+  const bool wmir = POL != 0 && i == 1 && g.west_bc;
+  const int nr = min(RBS_R, g.jm - j0 + 1);  // rows of this thread
+  // every load of the thread's rows first (a colour pass writes only its own
+  // colour and the mirror slots, which no load of the pass reads): the
+  // other colour's rows j0-1 .. j0+R (row j's N is row j+1's centre row, its
+  // S row j-1's), and per row its own cells, rhs, the rows (i+-1, j) and the
+  // T/B shift scalar -- slot t0-1 (parity 0; for q = 0 the previous row's
+  // last slot, in bounds) or t0+4 (parity 1; the next row's first slot for
+  // the last group)
+  float4 O[RBS_R + 2], C[RBS_R], RH[RBS_R], E[RBS_R], W[RBS_R];
+  float X[RBS_R];
+  O[0] = ld4(oth - khp);
+#pragma unroll
+  for (int r = 0; r < RBS_R; ++r) {
+    if (r < nr) {
+      const int ro = r * khp;
+      O[r + 1] = ld4(oth + ro);
+      C[r] = ld4(own + ro);
+      RH[r] = ld4(rh + ro);
+      E[r] = ld4(oth + ro + spi);
+      W[r] = ld4(oth + ro - spi);
+      X[r] = ld1(oth + ro + (((S0 + r) & 1) == 0 ? -1 : 4));
+      if (r == nr - 1) O[r + 2] = ld4(oth + ro + khp);  // the last row's N
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RBS_R; ++r) {
+    if (r >= nr) break;
+    const int j = j0 + r;
+    const int ro = r * khp;
+    float val[4];
+    if (((S0 + r) & 1) == 0) {
+      rbs_row<0>(cf, om, C[r], RH[r], E[r], W[r], O[r + 2], O[r], O[r + 1], X[r], in0, val, acc);
+    } else {
+      rbs_row<1>(cf, om, C[r], RH[r], E[r], W[r], O[r + 2], O[r], O[r + 1], X[r], in1, val, acc);
+      if (POL != 0 && q == 0) oth[ro] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
+    }
+    st4(own + ro, val[0], val[1], val[2], val[3]);
+    if (wmir) st4(oth + ro - spi, val[0], val[1], val[2], val[3]);  // W mirror: p[0,j,k] = p[1,j,k]
+    if (POL == 1) {  // even jm: p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k] (same colour)
+      if (j == 1) st4(own + ro + g.jm * khp, val[0], val[1], val[2], val[3]);
+      if (j == g.jm) st4(own + ro - g.jm * khp, val[0], val[1], val[2], val[3]);
+    }
+  }
+}
+
+// One colour pass (colour c) in place on the split arrays.
+// POL 0: stored halo; 1: press, even jm (y mirrors); 2: press, odd jm
+// (y halo rows refreshed before the pass).  Every thread's first row is
+// odd (1 + a multiple of RBS_R), so its parity (c + ig) & 1 is uniform per
+// block: one block-uniform branch picks the compiled parity.  The residual
+// is reduced per warp (one partial per warp, no block barrier: warps that
+// finish early leave).
+template <int POL>
+__global__ void __launch_bounds__(RBS_NT, RBS_MINB) k_sor_rbs(Geo g, SplitGeo sg, float* __restrict__ ps,
+                                                    const float* __restrict__ rs, SorC cf, float om, int c,
+                                                    double* __restrict__ partials) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // float4 group of the rows
+  const int i = blockIdx.z + 1;
+  const int j0 = 1 + (blockIdx.y * blockDim.y + threadIdx.y) * RBS_R;
   double acc = 0.0;
-  float4 cv[RBS_R], rel4[RBS_R];
-  int base[RBS_R];
-  bool act[RBS_R];
-  // all rows' loads are issued before the first store (a colour pass writes
-  // only its own colour and reads the other one: nothing aliases)
-#pragma unroll
-  for (int r = 0; r < RBS_R; ++r) {
-    const int j = (blockIdx.y * RBS_R + r) * blockDim.y + threadIdx.y + 1;
-    act[r] = j <= g.jm && q < sg.kh4;
-    base[r] = 0;
-    rel4[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    cv[r] = rel4[r];
-    if (!act[r]) continue;
-    const int s = (c + ig + j + 1) & 1;
-    const int t0 = 4 * q;
-    const int b = i * spi + j * khp + t0;
-    base[r] = b;
-    const float4 pc = *reinterpret_cast<const float4*>(own + b);
-    const float4 rh = *reinterpret_cast<const float4*>(rc + b);
-    const float4 mid = *reinterpret_cast<const float4*>(oth + b);
-    const float4 pe = efix ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(oth + b + spi);
-    const float4 pw = wfix ? pc : *reinterpret_cast<const float4*>(oth + b - spi);
-    const int jn = (POL == 1 && j == g.jm && !y_stored) ? 1 : j + 1;
-    const int js = (POL == 1 && j == 1 && !y_stored) ? g.jm : j - 1;
-    const float4 pn = *reinterpret_cast<const float4*>(oth + b + (jn - j) * khp);
-    const float4 pso = *reinterpret_cast<const float4*>(oth + b + (js - j) * khp);
-    // T/B: s = 0 -> T = mid[m], B = mid[m-1] (m = 0: slot t0-1);
-    //      s = 1 -> T = mid[m+1] (m = 3: slot t0+4), B = mid[m]
-    const int kf = 2 * t0 + s;  // k of the group's first cell
-    float extra = 0.0f;
-    if (s == 0 && t0 > 0) extra = oth[b - 1];
-    if (s == 1 && kf + 6 <= g.km) extra = oth[b + 4];
-    const float pcv[4] = {pc.x, pc.y, pc.z, pc.w};
-    const float md[4] = {mid.x, mid.y, mid.z, mid.w};
-    const float ev[4] = {pe.x, pe.y, pe.z, pe.w};
-    const float wv[4] = {pw.x, pw.y, pw.z, pw.w};
-    const float nv[4] = {pn.x, pn.y, pn.z, pn.w};
-    const float sv[4] = {pso.x, pso.y, pso.z, pso.w};
-    const float rv[4] = {rh.x, rh.y, rh.z, rh.w};
-    float out[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int k = kf + 2 * m;
-      out[m] = 0.0f;
-      if (k < 1 || k > g.km) continue;
-      float pT = s == 0 ? md[m] : (m < 3 ? md[m + 1] : extra);
-      float pB = s == 0 ? (m > 0 ? md[m - 1] : extra) : md[m];
-      if (POL == 1) {
-        if (k == g.km) pT = 0.0f;
-        if (k == 1) pB = pcv[m];
-      }
-      // sor.py:164-171: E, W, N, S, T, B summed left to right; sor.py:197
-      float nb = cf.w2l * ev[m];
-      nb = nb + cf.w2s * wv[m];
-      nb = nb + cf.w3l * nv[m];
-      nb = nb + cf.w3s * sv[m];
-      nb = nb + cf.w4l * pT;
-      nb = nb + cf.w4s * pB;
-      out[m] = om * (cf.cn1s * (nb - rv[m]) - pcv[m]);
-    }
-    cv[r] = pc;
-    rel4[r] = make_float4(out[0], out[1], out[2], out[3]);
+  if (q < sg.kh4 && j0 <= g.jm) {
+    const int off = i * (int)sg.spi + j0 * sg.khp + 4 * q;
+    float* own = ps + (long long)c * sg.n + off;
+    float* oth = ps + (long long)(c ^ 1) * sg.n + off;  // read; PRESS mirrors write W/B halo slots
+    const float* rh = rs + (long long)c * sg.n + off;
+    if (((c + i + g.ioff) & 1) == 0) rbs_march<POL, 0>(g, sg, own, oth, rh, cf, om, q, i, j0, acc);
+    else rbs_march<POL, 1>(g, sg, own, oth, rh, cf, om, q, i, j0, acc);
   }
-#pragma unroll
-  for (int r = 0; r < RBS_R; ++r) {
-    if (!act[r]) continue;
-    // non-interior slots (k halo, row padding) get rel = 0: p + 0 == p for
-    // every value, including -0.0 + 0.0?  No (-0 + 0 = +0): store them as read
-    const int j = (blockIdx.y * RBS_R + r) * blockDim.y + threadIdx.y + 1;
-    const int s = (c + ig + j + 1) & 1;
-    const int kf = 8 * q + s;
-    const float pcv[4] = {cv[r].x, cv[r].y, cv[r].z, cv[r].w};
-    const float rl[4] = {rel4[r].x, rel4[r].y, rel4[r].z, rel4[r].w};
-    float nv[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int k = kf + 2 * m;
-      const bool in = k >= 1 && k <= g.km;
-      nv[m] = in ? pcv[m] + rl[m] : pcv[m];
-      if (in) acc += (double)rl[m] * (double)rl[m];
-    }
-    *reinterpret_cast<float4*>(own + base[r]) = make_float4(nv[0], nv[1], nv[2], nv[3]);
-  }
-  // fixed-order block reduction
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   const int ltid = threadIdx.x + threadIdx.y * blockDim.x;
-  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
-  if ((ltid & 31) == 0) red[ltid >> 5] = acc;
+  if ((ltid & 31) == 0) {
+    const int wpb = (blockDim.x * blockDim.y + 31) >> 5;
+    const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    partials[blk * wpb + (ltid >> 5)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The same pass with the tiles staged in shared memory by TMA bulk copies
+// (cp.async.bulk, 1-D: every tile input is one contiguous run of the split
+// layout), so the bytes in flight do not live in registers.  A tile is
+// TR consecutive rows of one plane: its own cells and rhs (TR rows each),
+// the other colour's rows (i+-1, j0 .. j0+TR-1) and (i, j0-1 .. j0+TR) --
+// five copies, one mbarrier.  Persistent CTAs walk the tiles (plane-major,
+// so the CTAs in flight share their E/W planes through L2) with an NS-stage
+// ring: the copies of the next NS-1 tiles are in flight while a tile is
+// computed from shared memory.  A thread computes four slots of two
+// consecutive rows of a tile (TR even: the first row's parity is uniform
+// per tile), stores straight to global memory, and the CTA's residual is
+// reduced per warp at the end (fixed tile order: deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ float4 lds4(const float* a) { return *reinterpret_cast<const float4*>(a); }
+
+struct RbtPlan {
+  int rpt;     // rows per thread per tile (even)
+  int tr;      // rows per tile
+  int ns;      // pipeline stages
+  int ntj;     // tiles per plane
+  int ntiles;  // tiles per pass
+  int grid;    // persistent CTAs
+  int threads; // kh4 * tr / 2
+  size_t smem; // dynamic shared memory bytes
+};
+
+// stage layout (floats): own[tr*khp] rhs[tr*khp] E[tr*khp] W[tr*khp] mid[(tr+2)*khp]
+
+// Rows r0 .. r0+RPT-1 of a tile staged at st (RPT even: the first row's
+// parity S0 is the tile's).  o = float offset of the thread's first cell in
+// the colour arrays (32-bit: split_supported bounds the arrays).
+template <int POL, int S0, int RPT>
+__device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plane, int khp, int spi, float* own_g,
+                                         float* oth_g, const SorC& cf, float om, const bool (&in0)[4],
+                                         const bool (&in1)[4], bool lead, int i, int j, int o, int sro, int nr,
+                                         double& acc) {
+  const float* s_own = st + sro;
+  const float* s_rhs = s_own + plane;
+  const float* s_e = s_own + 2 * plane;
+  const float* s_w = s_own + 3 * plane;
+  const float* s_mid = s_own + 4 * plane + khp;  // the tile's mid rows start one row in (row -1 is staged)
+  const bool wmir = POL != 0 && i == 1 && g.west_bc;
+#pragma unroll
+  for (int h = 0; h < RPT; ++h) {
+    if (h >= nr) break;
+    const int ro = h * khp;
+    const float4 C = lds4(s_own + ro), RH = lds4(s_rhs + ro), E = lds4(s_e + ro), W = lds4(s_w + ro);
+    const float4 So = lds4(s_mid + ro - khp), M = lds4(s_mid + ro), N = lds4(s_mid + ro + khp);
+    float val[4];
+    const int go = o + ro;
+    if (((S0 + h) & 1) == 0) {
+      rbs_row<0>(cf, om, C, RH, E, W, N, So, M, s_mid[ro - 1], in0, val, acc);
+    } else {
+      rbs_row<1>(cf, om, C, RH, E, W, N, So, M, s_mid[ro + 4], in1, val, acc);
+      if (POL != 0 && lead) oth_g[go] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
+    }
+    st4(own_g + go, val[0], val[1], val[2], val[3]);
+    if (wmir) st4(oth_g + go - spi, val[0], val[1], val[2], val[3]);  // W mirror: p[0,j,k] = p[1,j,k]
+    if (POL == 1) {  // even jm: p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k] (same colour)
+      if (j + h == 1) st4(own_g + go + g.jm * khp, val[0], val[1], val[2], val[3]);
+      if (j + h == g.jm) st4(own_g + go - g.jm * khp, val[0], val[1], val[2], val[3]);
+    }
+  }
+}
+
+template <int POL, int RPT>
+__global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __restrict__ ps,
+                                                 const float* __restrict__ rs, SorC cf, float om, int c, RbtPlan pl,
+                                                 double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
+  float* stages = reinterpret_cast<float*>(smem_raw + 128);
+  const int khp = sg.khp;
+  const int spi = (int)sg.spi;
+  const int plane = pl.tr * khp;
+  const int sfl = (5 * pl.tr + 2) * khp;
+  float* own_g = ps + (long long)c * sg.n;
+  float* oth_g = ps + (long long)(c ^ 1) * sg.n;
+  const float* rhs_g = rs + (long long)c * sg.n;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < pl.ns; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
-  if (ltid == 0) {
-    double sum = 0.0;
-    for (int w = 0; w < nw; ++w) sum += red[w];
-    partials[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = sum;
+  // tile t (plane-major): plane 1 + t / ntj, rows from 1 + (t % ntj) * tr;
+  // the CTA walks t = blockIdx.x + k * gridDim.x with incremental (i, jt)
+  const int di = (int)gridDim.x / pl.ntj, djt = (int)gridDim.x % pl.ntj;
+  auto issue = [&](int i, int jt, int s) {
+    const int j0 = 1 + jt * pl.tr;
+    const int nrow = min(pl.tr, g.jm - j0 + 1);
+    const unsigned rb = (unsigned)(nrow * khp * 4);
+    float* st = stages + s * sfl;
+    const int go = i * spi + j0 * khp;
+    mbar_expect_tx(&bar[s], 4 * rb + rb + 2u * khp * 4);
+    bulk_g2s(st, own_g + go, rb, &bar[s]);
+    bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
+    bulk_g2s(st + 2 * plane, oth_g + go + spi, rb, &bar[s]);
+    bulk_g2s(st + 3 * plane, oth_g + go - spi, rb, &bar[s]);
+    bulk_g2s(st + 4 * plane, oth_g + go - khp, rb + 2u * khp * 4, &bar[s]);
+  };
+  const int my = (pl.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
+  int ii = 1 + (int)blockIdx.x / pl.ntj, jt = (int)blockIdx.x % pl.ntj;  // tile k of the compute loop
+  if (tid == 0) {
+    int pi = ii, pj = jt;
+    for (int k = 0; k < pl.ns && k < my; ++k) {
+      issue(pi, pj, k);
+      pi += di;
+      pj += djt;
+      if (pj >= pl.ntj) { pj -= pl.ntj; ++pi; }
+    }
+  }
+  // the issue cursor runs ns tiles ahead of the compute cursor
+  int ni = ii, nj = jt;
+  for (int k = 0; k < pl.ns; ++k) {
+    ni += di;
+    nj += djt;
+    if (nj >= pl.ntj) { nj -= pl.ntj; ++ni; }
+  }
+  // per-thread invariants: its slot group q, its rows r0 .. r0+RPT-1 of a tile
+  const int q = threadIdx.x, r0 = RPT * threadIdx.y;
+  bool in0[4], in1[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int k0 = 8 * q + 2 * m;
+    in0[m] = k0 >= 1 && k0 <= g.km;
+    in1[m] = k0 + 1 <= g.km;
+  }
+  const bool lead = q == 0;
+  const int sro = r0 * khp + 4 * q;  // the thread's offset inside a staged array
+  double acc = 0.0;
+  for (int k = 0; k < my; ++k) {
+    const int s = k % pl.ns;
+    mbar_wait(&bar[s], (unsigned)((k / pl.ns) & 1));
+    const int j = 1 + jt * pl.tr + r0;
+    const int nr = g.jm - j + 1;  // rows left in the plane from the thread's first row
+    if (nr > 0) {
+      const int o = ii * spi + j * khp + 4 * q;
+      const float* st = stages + s * sfl;
+      if (((c + ii + g.ioff) & 1) == 0)
+        rbt_rows<POL, 0, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, ii, j, o, sro, nr, acc);
+      else
+        rbt_rows<POL, 1, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, ii, j, o, sro, nr, acc);
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0 && k + pl.ns < my) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async overwrite
+      issue(ni, nj, s);
+    }
+    ii += di;
+    jt += djt;
+    if (jt >= pl.ntj) { jt -= pl.ntj; ++ii; }
+    ni += di;
+    nj += djt;
+    if (nj >= pl.ntj) { nj -= pl.ntj; ++ni; }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) {
+    const int wpb = (blockDim.x * blockDim.y + 31) >> 5;
+    partials[(long long)blockIdx.x * wpb + (tid >> 5)] = acc;
   }
 }
 
@@ -208,8 +462,7 @@ __global__ void k_split_refresh_y(Geo g, SplitGeo sg, float* __restrict__ ps, in
 
 // Merge the split p back into the natural layout: a warp per natural row,
 // lanes over k.  PRESS: halo cells (not on a neighbour slab's plane) take
-// the closed-form halo_fn source (k: 0 -> 1, km+1 -> 0; then j periodic;
-// then i: 0 -> 1, im+1 -> 0), which reproduces the reference's final
+// the closed-form halo_fn source, which reproduces the reference's final
 // _pressure_halo call; STORED: every cell as stored.  flags: the press
 // stage's non-finite check over the whole result.
 template <int POL>
@@ -247,31 +500,113 @@ __global__ void __launch_bounds__(256) k_split_unpack(Geo g, SplitGeo sg, const 
 
 }  // namespace
 
-void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, cudaStream_t st) {
+void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st) {
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
-  k_split_pack<<<(unsigned)((nrow + 7) / 8), 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n);
+  const unsigned nb = (unsigned)((nrow + 7) / 8);
+  if (policy == 1) k_split_pack<1><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n);
+  else k_split_pack<0><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n);
 }
 
-int sor_blocks_split(const Geo& g) {
+static dim3 rbs_grid(const Geo& g, const SplitGeo& sg, int* bx, int* by) {
+  rbs_shape(sg, bx, by);
+  return dim3((sg.kh4 + *bx - 1) / *bx, (g.jm + *by * RBS_R - 1) / (*by * RBS_R), g.im);
+}
+
+// LESB_SPLIT_REG=1: the register-staged pass kernel (k_sor_rbs) instead of
+// the TMA-staged one (A/B experiments)
+static bool use_reg_kernel() {
+  static const int v = [] {
+    const char* e = std::getenv("LESB_SPLIT_REG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// Tile plan of the TMA pass: ~256 threads (two rows each) per tile, two
+// stages, as many CTAs per SM as fit (occupancy query: two at km = 90),
+// persistent.  Measured at 512x512x90 (stored / press, us per iteration):
+// 42 rows x 2 stages 74.5 / 80.9; 20 x 3: 77.7 / 86.8; 30 x 3: 78.5 / 87.1;
+// 42 x 3 (one CTA per SM): 93.8 / 105.8; 10 x 4: 94.0 / 103.0.
+static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
+  RbtPlan pl{};
+  static const int env_tr = std::getenv("LESB_RBT_TR") ? std::atoi(std::getenv("LESB_RBT_TR")) : 0;
+  static const int env_ns = std::getenv("LESB_RBT_NS") ? std::atoi(std::getenv("LESB_RBT_NS")) : 0;
+  static const int env_rpt = std::getenv("LESB_RBT_RPT") ? std::atoi(std::getenv("LESB_RBT_RPT")) : 0;
+  const int rpt = env_rpt == 4 ? 4 : 2;
+  int tr = env_tr > 0 ? env_tr : rpt * (512 / (2 * sg.kh4));
+  tr = std::max(rpt, tr - tr % rpt);
+  while (tr > rpt && sg.kh4 * (tr / rpt) > 512) tr -= rpt;
+  const size_t stage = (size_t)(5 * tr + 2) * sg.khp * sizeof(float);
+  int ns = env_ns > 0 ? env_ns : 2;
+  while (ns > 2 && 128 + ns * stage > 200 * 1024) --ns;
+  pl.rpt = rpt;
+  pl.tr = tr;
+  pl.ns = ns;
+  pl.threads = sg.kh4 * (tr / rpt);
+  pl.smem = 128 + ns * stage;
+  pl.ntj = (g.jm + tr - 1) / tr;
+  pl.ntiles = pl.ntj * g.im;
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sor_rbt<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  if (rpt == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 4>, pl.threads, pl.smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 2>, pl.threads, pl.smem);
+  if (per < 1) per = 1;
+  pl.grid = std::min(pl.ntiles, sms * per);
+  return pl;
+}
+
+static bool rbt_ok(const SplitGeo& sg) { return sg.kh4 <= 512 && !use_reg_kernel(); }
+
+int sor_blocks_split(const Geo& g) {  // residual partials per pass: one per warp
   const SplitGeo sg = split_geo(g);
+  if (rbt_ok(sg)) {
+    const RbtPlan pl = rbt_plan(g, sg);
+    return pl.grid * ((pl.threads + 31) / 32);
+  }
   int bx, by;
-  rbs_shape(sg, &bx, &by);
-  return ((sg.kh4 + bx - 1) / bx) * ((g.jm + by * RBS_R - 1) / (by * RBS_R)) * g.im;
+  const dim3 gr = rbs_grid(g, sg, &bx, &by);
+  return gr.x * gr.y * gr.z * ((bx * by + 31) / 32);
 }
 
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
                      cudaStream_t st) {
   const SplitGeo sg = split_geo(g);
+  float* rs = split + 2 * sg.n;
+  const int pol = policy == 1 ? ((g.jm & 1) ? 2 : 1) : 0;
+  if (pol == 2)  // odd jm: the y halo rows are a pre-pass snapshot
+    k_split_refresh_y<<<dim3((sg.khp + 127) / 128, g.im), 128, 0, st>>>(g, sg, split, c);
+  if (rbt_ok(sg)) {
+    const RbtPlan pl = rbt_plan(g, sg);
+    const dim3 block(sg.kh4, pl.tr / pl.rpt);
+    if (pl.rpt == 4) {
+      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+    } else {
+      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+    }
+    return;
+  }
   int bx, by;
-  rbs_shape(sg, &bx, &by);
-  const int y_stored = (policy == 1 && (g.jm & 1)) ? 1 : 0;
-  if (y_stored) k_split_refresh_y<<<dim3((sg.khp + 127) / 128, g.im), 128, 0, st>>>(g, sg, split, c);
-  dim3 grid((sg.kh4 + bx - 1) / bx, (g.jm + by * RBS_R - 1) / (by * RBS_R), g.im);
-  if (policy == 1)
-    k_sor_rbs<1><<<grid, dim3(bx, by), 0, st>>>(g, sg, split, split + 2 * sg.n, cf, om, c, y_stored, partials);
-  else
-    k_sor_rbs<0><<<grid, dim3(bx, by), 0, st>>>(g, sg, split, split + 2 * sg.n, cf, om, c, 0, partials);
+  const dim3 grid = rbs_grid(g, sg, &bx, &by);
+  const dim3 block(bx, by);
+  if (pol == 2) k_sor_rbs<2><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
+  else if (pol == 1) k_sor_rbs<1><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
+  else k_sor_rbs<0><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
 }
 
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st) {
