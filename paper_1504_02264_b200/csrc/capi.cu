@@ -112,6 +112,7 @@ struct lesb_domain {
   int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 natural-layout passes
   float* split = nullptr;  // colour-split p / rhs of the streaming red-black passes (4 * SplitGeo::n floats)
   void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
+  int* coll_d = nullptr;      // NCCL slabs: scratch of the stage reductions
   unsigned* repoch = nullptr;  // resident solver tag epoch
   // x-slab on NCCL ranks: the neighbour ranks' face buffers mapped through
   // CUDA IPC (peer memory over NVLink) so the resident solver exchanges tile
@@ -209,7 +210,10 @@ bool map_slab_peers(lesb_domain* h) {
     cudaIpcMemHandle_t h;
     long long im, jm, km, words, ok;
   } rec{};
-  rec.ok = cudaIpcGetMemHandle(&rec.h, h->xbuf) == cudaSuccess;
+  // a rank without a face buffer (its slab does not fit the resident plan,
+  // or another LESB_SOR_PATH) still takes part in both collectives and
+  // votes "not mapped", so every rank keeps the streaming passes
+  rec.ok = h->xbuf != nullptr && cudaIpcGetMemHandle(&rec.h, h->xbuf) == cudaSuccess;
   rec.im = h->g.im;
   rec.jm = h->g.jm;
   rec.km = h->g.km;
@@ -264,7 +268,7 @@ int ensure_partials(lesb_domain* h, int n_iter) {
     CK(cudaMalloc(&h->repoch, sizeof(unsigned)));
     CK(cudaMemset(h->repoch, 0, sizeof(unsigned)));
   }
-  if (h->link.comm && h->xbuf && !h->peer_tried) {
+  if (h->link.comm && !h->peer_tried) {  // collective: every rank, whatever its own plan
     h->peer_tried = true;
     map_slab_peers(h);  // on failure the slab keeps the streaming colour passes
   }
@@ -361,6 +365,27 @@ void local_exchange(lesb_domain* h, float* lesb_domain::*which, int depth, cudaS
 void nccl_p_hook(void* ctx, float* p, long long plane) {
   lesb_domain* h = static_cast<lesb_domain*>(ctx);
   nccl_exchange(h, p, 1, h->st, plane);
+}
+
+// NCCL slabs: reductions over the ranks on the domain stream, synchronous
+// (SURVEY 8(e) C4, C5).  coll_d: 2 ints of scratch.
+int nccl_int_reduce(lesb_domain* h, int* v, ncclRedOp_t op) {
+  if (!h->coll_d) CK(cudaMalloc(&h->coll_d, 2 * sizeof(int)));
+  CK(cudaMemcpyAsync(h->coll_d, v, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  if (ncclAllReduce(h->coll_d, h->coll_d + 1, 1, ncclInt, op, h->link.comm, h->st) != ncclSuccess)
+    return fail(LESB_E_CUDA, "ncclAllReduce (stage reduction) failed");
+  CK(cudaMemcpyAsync(v, h->coll_d + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return LESB_OK;
+}
+
+// C4: the residual history is the sum of the slabs' partial histories
+// (in place on res_d; only when the caller asks for residuals -- inside a
+// step nothing reads them)
+int nccl_residuals(lesb_domain* h, int n_iter) {
+  if (ncclAllReduce(h->res_d, h->res_d, n_iter, ncclDouble, ncclSum, h->link.comm, h->st) != ncclSuccess)
+    return fail(LESB_E_CUDA, "ncclAllReduce (residuals) failed");
+  return LESB_OK;
 }
 
 // in-process neighbours, one colour array of the split layout: planes 0 and
@@ -501,10 +526,21 @@ int check_args_step(lesb_domain* h, int n_iter, int scheme) {
 // runs and the check after it raises (velnw can never clear a non-finite).
 int handle_dirty_state(lesb_domain* h, int* fail_stage, bool* failed) {
   *failed = false;
-  if (h->known_finite) return LESB_OK;
-  bool ok = false;
-  int rc = scan_finite(h, &ok);
-  if (rc) return rc;
+  bool ok = true;
+  if (!h->known_finite) {
+    int rc = scan_finite(h, &ok);
+    if (rc) return rc;
+  }
+  // NCCL slabs decide together (a rank returning early would strand the
+  // others' exchanges).  SPMD contract: every rank makes the same calls, so
+  // known_finite -- made global after every step by the stage reduction --
+  // is the same on every rank and they all reach this collective together.
+  if (h->link.comm && !h->known_finite) {
+    int bad = ok ? 0 : 1;
+    int rc = nccl_int_reduce(h, &bad, ncclMax);
+    if (rc) return rc;
+    ok = bad == 0;
+  }
   if (!ok) {
     launch_velnw(h->g, h->spac(), h->u, h->v, h->w, h->p, h->fgh, h->dt, h->st);
     CK(cudaStreamSynchronize(h->st));
@@ -612,6 +648,7 @@ int lesb_destroy(lesb_handle h) {
   if (h->gxbuf) cudaFree(h->gxbuf);
   if (h->gepoch) cudaFree(h->gepoch);
   if (h->split) cudaFree(h->split);
+  if (h->coll_d) cudaFree(h->coll_d);
   if (h->res_d) cudaFree(h->res_d);
   if (h->book_d) cudaFree(h->book_d);
   if (h->res_h) cudaFreeHost(h->res_h);
@@ -805,6 +842,10 @@ int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* resid
   if (rc) return rc;
   CK(enqueue_press(h, n_iter, scheme, omega, true, nullptr));
   CK(cudaGetLastError());
+  if (residuals_out && h->link.comm) {
+    rc = nccl_residuals(h, n_iter);
+    if (rc) return rc;
+  }
   if (residuals_out)
     CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -825,9 +866,16 @@ int lesb_sor_solve(lesb_handle h, int n_iter, int scheme, float omega, int halo_
   if (scheme == LESB_TWINNED)
     CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
   ResidentBufs rb = h->rbufs();
+  const bool res_slab = h->link.comm && rb.use && scheme == LESB_REDBLACK;
+  ExchangeHook hook{h->link.comm && !res_slab ? nccl_p_hook : nullptr, h};
   CK(enqueue_sor(h->g, h->p, h->pb, h->rhs, h->sorc(), omega, n_iter, scheme, halo_policy, h->partials, h->res_d,
-                 nullptr, h->st, nullptr, nullptr, &rb));
+                 nullptr, h->st, &hook, nullptr, &rb));
+  if (res_slab) nccl_exchange(h, h->p, 1, h->st);  // inner x halo planes: the final values
   CK(cudaGetLastError());
+  if (residuals_out && h->link.comm) {
+    rc = nccl_residuals(h, n_iter);
+    if (rc) return rc;
+  }
   if (residuals_out)
     CK(cudaMemcpyAsync(residuals_out, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -859,12 +907,22 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
   CK(cudaGraphLaunch(ge, h->st));
   CK(cudaStreamSynchronize(h->st));
+  if (residuals_out && h->link.comm) {  // C4: the global residual history
+    rc = nccl_residuals(h, n_iter);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
   if (residuals_out) std::memcpy(residuals_out, h->res_h, n_iter * sizeof(double));
   if (h->book_h->err) return resident_timeout(h);
-  unsigned bits = h->book_h->flags;
-  if (bits) {
+  int stage = h->book_h->flags ? first_stage(h->book_h->flags) : 99;
+  if (h->link.comm) {  // C5: the first failing stage anywhere in the grid (step order), on every rank
+    rc = nccl_int_reduce(h, &stage, ncclMin);
+    if (rc) return rc;
+  }
+  if (stage < 99) {
     h->known_finite = false;
-    if (fail_stage) *fail_stage = first_stage(bits);
+    if (fail_stage) *fail_stage = stage;
     return LESB_NONFINITE;
   }
   return LESB_OK;
@@ -1043,11 +1101,19 @@ int lesb_kernels_per_step(lesb_handle h, int n_iter, int scheme) {
 
 namespace {
 
-int get_solver(int im, int jm, int km, int device, lesb_domain** out) {
+// Solver domains for the host-buffer entry points, cached per (shape,
+// device).  Cached domains are never destroyed while the library is loaded
+// (a caller on another thread may hold one); once the cache holds
+// kMaxSolvers shapes, further shapes get a private domain that the call
+// destroys when it returns.
+constexpr size_t kMaxSolvers = 8;
+
+int get_solver(int im, int jm, int km, int device, lesb_domain** out, bool* owned) {
   std::lock_guard<std::mutex> lk(g_solver_mu_fwd());
   auto& g_solvers = solver_map();
   auto key = std::make_tuple(im, jm, km, device);
   auto it = g_solvers.find(key);
+  *owned = false;
   if (it != g_solvers.end()) {
     *out = it->second;
     return LESB_OK;
@@ -1061,28 +1127,29 @@ int get_solver(int im, int jm, int km, int device, lesb_domain** out) {
   lesb_domain* h = nullptr;
   int rc = lesb_create(&d, &h);
   if (rc) return rc;
-  // keep at most a handful of solver contexts alive
-  if (g_solvers.size() >= 8) {
-    lesb_destroy(g_solvers.begin()->second);
-    g_solvers.erase(g_solvers.begin());
-  }
-  g_solvers[key] = h;
+  if (g_solvers.size() < kMaxSolvers) g_solvers[key] = h;
+  else *owned = true;
   *out = h;
   return LESB_OK;
 }
 
-int solver_prepare(int im, int jm, int km, const float* rhs, const lesb_coeffs* c, int device, lesb_domain** out) {
+// destroys a private (uncached) solver domain at scope exit
+struct SolverLease {
+  lesb_domain* h = nullptr;
+  bool owned = false;
+  ~SolverLease() {
+    if (owned && h) lesb_destroy(h);
+  }
+};
+
+int solver_prepare(int im, int jm, int km, const float* rhs, const lesb_coeffs* c, int device, SolverLease* out) {
   if (im < 1 || jm < 1 || km < 1) return fail(LESB_E_ARG, "grid dimensions must be >= 1");
   if (!rhs || !c) return fail(LESB_E_ARG, "null argument");
-  lesb_domain* h = nullptr;
-  int rc = get_solver(im, jm, km, device, &h);
+  int rc = get_solver(im, jm, km, device, &out->h, &out->owned);
   if (rc) return rc;
-  rc = lesb_set_coeffs(h, c);
+  rc = lesb_set_coeffs(out->h, c);
   if (rc) return rc;
-  rc = lesb_upload(h, LESB_RHS, rhs);
-  if (rc) return rc;
-  *out = h;
-  return LESB_OK;
+  return lesb_upload(out->h, LESB_RHS, rhs);
 }
 
 }  // namespace
@@ -1096,9 +1163,10 @@ int lesb_solve_pressure(int im, int jm, int km, const float* p0, const float* rh
   if (scheme != LESB_REDBLACK && scheme != LESB_TWINNED) return fail(LESB_E_ARG, "unknown scheme");
   if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
   if (!p0 || !p_out) return fail(LESB_E_ARG, "null argument");
-  lesb_domain* h = nullptr;
-  int rc = solver_prepare(im, jm, km, rhs, c, device, &h);
+  SolverLease lease;
+  int rc = solver_prepare(im, jm, km, rhs, c, device, &lease);
   if (rc) return rc;
+  lesb_domain* h = lease.h;
   std::lock_guard<std::mutex> lk(h->mu);
   CK(cudaSetDevice(h->device));
   rc = ensure_partials(h, n_iter);
@@ -1124,9 +1192,10 @@ int lesb_redblack_iteration(int im, int jm, int km, float* p, const float* rhs, 
 int lesb_twinned_sweep(int im, int jm, int km, const float* src, float* dst, const float* rhs, const lesb_coeffs* c,
                        float omega, double* residual, int device) {
   if (!src || !dst) return fail(LESB_E_ARG, "null argument");
-  lesb_domain* h = nullptr;
-  int rc = solver_prepare(im, jm, km, rhs, c, device, &h);
+  SolverLease lease;
+  int rc = solver_prepare(im, jm, km, rhs, c, device, &lease);
   if (rc) return rc;
+  lesb_domain* h = lease.h;
   std::lock_guard<std::mutex> lk(h->mu);
   CK(cudaSetDevice(h->device));
   rc = ensure_partials(h, 1);

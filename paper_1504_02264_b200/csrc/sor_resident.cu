@@ -52,6 +52,15 @@
 
 namespace cg = cooperative_groups;
 
+// Timing experiments that drop waits / updates / receives (results wrong):
+// compiled only into experiment builds (scripts/build_variant.sh NAME WORK
+// -DLESB_RES_DEBUG_BUILD), never into the product library.
+#ifdef LESB_RES_DEBUG_BUILD
+#define RES_DBG(a, bit) ((a).debug & (bit))
+#else
+#define RES_DBG(a, bit) 0
+#endif
+
 namespace lesb {
 
 constexpr int RES_THREADS = 512;
@@ -659,7 +668,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   // the receive loads of pass n (register-held pairs), issued during pass n-1
   unsigned long long v[RCVP][2];
   auto issue_receive = [&](int n) {
-    if (a.debug & 4) return;
+    if (RES_DBG(a, 4)) return;
     const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
     const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
     const unsigned vm = ((n & 1) ? rval1 : rval0) & (n == 1 ? ~rwrapm : ~0u);
@@ -678,7 +687,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     // slots: pass n-1's publish, or pass n-2's across an odd-jm periodic wrap.
     // Those slots were last read in pass n-2, which every thread finished
     // before the barrier of pass n-1, so no barrier is needed before this.
-    if (n > 0 && !(a.debug & 4)) {
+    if (n > 0 && !RES_DBG(a, 4)) {
       const unsigned long long* XB1 = a.xbuf + ((n + 3) & 3) * bstride;
       const unsigned long long* XB2 = a.xbuf + ((n + 2) & 3) * bstride;
       const unsigned t1 = tag0 + (unsigned)(n + 1), t2 = tag0 + (unsigned)n;
@@ -692,7 +701,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
         for (int h = 0; h < 2; ++h) {
           if (!((vm >> (2 * u + h)) & 1u)) continue;
           unsigned spins = 0;
-          while ((unsigned)(v[u][h] >> 32) != want && !timed_out && !(a.debug & 1)) {
+          while ((unsigned)(v[u][h] >> 32) != want && !timed_out && !RES_DBG(a, 1)) {
             if (++spins > (1u << 24)) {  // ~seconds: never hang the GPU
               atomicOr(a.err, 1u);
               timed_out = true;
@@ -727,7 +736,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
           const unsigned long long* src = (w2 ? XB2 : XB1) + e.y + sl;
           unsigned long long x = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
           unsigned spins = 0;
-          while ((unsigned)(x >> 32) != want && !timed_out && !(a.debug & 1)) {
+          while ((unsigned)(x >> 32) != want && !timed_out && !RES_DBG(a, 1)) {
             if (++spins > (1u << 24)) {
               atomicOr(a.err, 1u);
               timed_out = true;
@@ -745,11 +754,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     if (nrd == 0) acc = 0.0;  // one residual per iteration: both colour passes
     unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
     unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
-    if (!(a.debug & 2))
+    if (!RES_DBG(a, 2))
       acc += update_boundary<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, bc0, bj0, bdq, bdr, nbnd, HPb, nrd,
                                          KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
-    if (!(a.debug & 2))
+    if (!RES_DBG(a, 2))
       acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, idg, idcc, L_i, KT, nrd, KK, CW, sI, km,
                                  [&] {
                                    if (n + 1 < 2 * a.n_iter) issue_receive(n + 1);
@@ -1011,8 +1020,12 @@ static ResArgs make_args(const ResidentCall& c, const ResPlan& pl) {
   a.err = c.err;
   a.peer_w = (unsigned long long*)c.peer_w;
   a.peer_e = (unsigned long long*)c.peer_e;
+#ifdef LESB_RES_DEBUG_BUILD
   static const int dbg = getenv("LESB_RES_DEBUG") ? atoi(getenv("LESB_RES_DEBUG")) : 0;
   a.debug = dbg;
+#else
+  a.debug = 0;
+#endif
   a.trace = nullptr;
   a.book = c.book;
   return a;

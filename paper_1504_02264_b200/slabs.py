@@ -24,7 +24,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as N
-from .les import _FIELD_ID, _csd2, _inflow_arrays, _scheme_code
+from .les import _FIELD_ID, _check_solver_args, _csd2, _inflow_arrays, _scheme_code
 from .reftypes import Grid, NumericsError, Scheme, is_redblack
 from .sor import build_uniform_coeffs
 
@@ -108,7 +108,8 @@ class _Slab:
 
     def upload(self, name, global_arr):
         part = slice_global(np.asarray(global_arr, np.float32), self.i0, self.i1)
-        N.check(self.lib.lesb_upload(self.h, _FIELD_ID[name], N.fptr(part)), "lesb_upload")
+        fid = N.LESB_RHS if name == "rhs" else _FIELD_ID[name]
+        N.check(self.lib.lesb_upload(self.h, fid, N.fptr(part)), "lesb_upload")
 
     def download(self, name, jm, km):
         shape = (self.im + 2, jm + 2, km + 2) + ((3,) if name in ("fgh", "fgh_old") else ())
@@ -185,25 +186,57 @@ class SlabDomain:
         for name in FIELDS:
             self.slab.upload(name, state[name])
 
-    def step(self, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK) -> None:
-        """One step; every rank raises the same NumericsError (stage bits are
-        OR-reduced over ranks)."""
-        import torch
-
+    def step(self, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK, residuals: bool = False):
+        """One step (les.py:393-416) on every rank.  The library reduces the
+        first failing stage over the ranks with NCCL, so
+        every rank raises the same NumericsError; with ``residuals`` the
+        press residual history is the NCCL sum over the slabs (C4)."""
         g = self.grid
         arrs = _inflow_arrays(inflow, g.km)
         stage = N.C.c_int(-1)
         omega = 1.7 if is_redblack(scheme) else 1.0
+        res = np.zeros(n_iter, np.float64) if residuals else None
         rc = N.check(self.slab.lib.lesb_step(self.slab.h, *[N.fptr(a) for a in arrs], int(n_iter),
-                                             _scheme_code(scheme), float(omega), None, N.C.byref(stage)),
+                                             _scheme_code(scheme), float(omega), N.dptr(res), N.C.byref(stage)),
                      "lesb_step")
-        # the reference raises after the first stage (in step order) that left a
-        # non-finite value anywhere in the grid: the minimum over ranks
-        dev = "cuda" if self.dist.get_backend() == "nccl" else "cpu"
-        first = torch.tensor([stage.value if rc == N.LESB_NONFINITE else 99], dtype=torch.int64, device=dev)
-        self.dist.all_reduce(first, op=self.dist.ReduceOp.MIN)
-        if int(first.item()) < 99:
-            raise NumericsError(N.STAGE_NAMES[int(first.item())], "device stage check (slabs)")
+        if rc == N.LESB_NONFINITE:
+            raise NumericsError(N.STAGE_NAMES[stage.value], "device stage check (slabs)")
+        return res
+
+    def press(self, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK, omega: float | None = None) -> np.ndarray:
+        """press (les.py:358-381) on the slabs: rhs from the slab's
+        velocities, SOR with the press halo and the per-pass plane exchange;
+        returns the global residual history (NCCL sum, C4) on every rank."""
+        if omega is None:
+            omega = 1.7 if is_redblack(scheme) else 1.0
+        res = np.zeros(n_iter, np.float64)
+        N.check(self.slab.lib.lesb_press(self.slab.h, int(n_iter), _scheme_code(scheme), float(omega), N.dptr(res)),
+                "lesb_press")
+        return res
+
+    def solve(self, p0: np.ndarray, rhs: np.ndarray, omega: float, n_iter: int, scheme: Scheme = Scheme.REDBLACK,
+              halo_policy: int = 0):
+        """solve_pressure (sor.py:255-309) decomposed over the ranks: every
+        rank passes the GLOBAL p0 and rhs (as sor-bench builds them), solves
+        its slab, and gets its slab of p (global planes i0-1 .. i1+1) and the
+        global residual history (NCCL sum over the slabs)."""
+        _check_solver_args(n_iter, scheme, 1)
+        self.slab.upload("p", p0)
+        self.slab.upload("rhs", rhs)
+        res = np.zeros(n_iter, np.float64)
+        N.check(self.slab.lib.lesb_sor_solve(self.slab.h, int(n_iter), _scheme_code(scheme), float(omega),
+                                             int(halo_policy), N.dptr(res)), "lesb_sor_solve")
+        return self.slab.download("p", self.grid.jm, self.grid.km), res
+
+    def gather(self, name: str):
+        """The global array of a field on rank 0 (None elsewhere): every
+        rank's slab travels to rank 0 (for dumps)."""
+        part = self.slab.download(name, self.grid.jm, self.grid.km)
+        parts = [None] * self.nranks if self.rank == 0 else None
+        self.dist.gather_object(part, parts, dst=0)
+        if self.rank != 0:
+            return None
+        return gather(parts, self.bounds)
 
     def close(self):
         self.slab.close()
