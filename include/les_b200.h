@@ -210,6 +210,11 @@ int lesb_link_nccl(lesb_handle h, const void* unique_id, int nranks, int rank);
 int lesb_link_local(lesb_handle* hs, int n);
 int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v, const float* in_w, int n_iter,
                     int scheme, float omega, double* residuals_out, int* fail_stage);
+/* solve_pressure (sor.py:255-309) on in-process slabs: each slab's p / rhs
+ * (LESB_P, LESB_RHS uploads) solved together; residuals = the sum of the
+ * slabs' histories.  sor-bench's x-slab table (cli.py:222-283). */
+int lesb_group_sor_solve(lesb_handle* hs, int n, int n_iter, int scheme, float omega, int halo_policy,
+                         double* residuals_out);
 
 #ifdef __cplusplus
 }

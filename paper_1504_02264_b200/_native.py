@@ -71,6 +71,7 @@ _SIGS = {
     "lesb_link_nccl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "lesb_link_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "lesb_group_step": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, FP, FP, FP, C.c_int, C.c_int, C.c_float, DP, IP]),
+    "lesb_group_sor_solve": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, DP]),
     "lesb_sor_solve": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_int, DP]),
     "lesb_step": (C.c_int, [C.c_void_p, FP, FP, FP, C.c_int, C.c_int, C.c_float, DP, IP]),
     "lesb_run_steps": (C.c_int, [C.c_void_p, C.c_int, FP, C.c_int, C.c_int, C.c_int, C.c_float, IP, IP]),

@@ -40,11 +40,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
+def nccl_flags():
+    """Link the NCCL that torch itself loads (the nvidia-nccl wheel, 2.28.x,
+    with an rpath to it): a process that imports torch and this library then
+    has one libnccl.so.2, whichever of the two is loaded first.  Falls back
+    to the system NCCL when the wheel is absent."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            lib, inc = os.path.join(d, "lib"), os.path.join(d, "include")
+            if os.path.exists(os.path.join(lib, "libnccl.so.2")) and os.path.exists(os.path.join(inc, "nccl.h")):
+                return ["-I", inc], ["-L", lib, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
+    except Exception:  # noqa: BLE001
+        pass
+    return [], ["-lnccl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"),
-           "-o", LIB + ".tmp", *sources(), "-lnccl"]
+    nccl_inc, nccl_lib = nccl_flags()
+    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), *nccl_inc,
+           "-o", LIB + ".tmp", *sources(), *nccl_lib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

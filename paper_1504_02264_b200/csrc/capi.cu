@@ -1264,6 +1264,130 @@ int lesb_link_local(lesb_handle* hs, int n) {
   return LESB_OK;
 }
 
+// The SOR solve of n in-process slabs on h0's stream (policy 1: press
+// halo, 0: stored halo), residual histories left in each slab's res_h and
+// flags in book_h (synchronised).  Red-black on slabs of one shape that fit:
+// the resident solver for the whole group in one cooperative launch;
+// otherwise the streaming passes (colour-split layout where supported) with
+// a plane copy after every pass / sweep.
+static int group_sor(lesb_domain** hs, int n, int n_iter, int scheme, float omega, int policy, cudaStream_t st) {
+  lesb_domain* h0 = hs[0];
+  // Red-black on slabs of one shape: the resident solver for the whole group
+  // in one cooperative launch, tile faces crossing slab boundaries through
+  // the neighbours' ghost slots (the in-process form of the NVLink peer path)
+  bool group_res = scheme == LESB_REDBLACK && n <= resident_group_max() &&
+                   (h0->sor_path == 0 || h0->sor_path == 2) && !std::getenv("LESB_GROUP_PASSES");
+  for (int s = 0; s < n && group_res; ++s)
+    group_res = hs[s]->g.im == h0->g.im && hs[s]->g.jm == h0->g.jm && hs[s]->g.km == h0->g.km &&
+                resident_supported(hs[s]->g, hs[s]->sorc(), hs[s]->device, resident_group_tiles(n));
+  if (group_res) {
+    for (int s = 0; s < n; ++s) {
+      lesb_domain* h = hs[s];
+      if (!h->gxbuf) {
+        const size_t xb = resident_xbuf_words(h->g, h->device, resident_group_tiles(n)) * sizeof(unsigned long long);
+        CK(cudaMalloc(&h->gxbuf, xb));
+        CK(cudaMemset(h->gxbuf, 0, xb));
+        CK(cudaMalloc(&h->gepoch, sizeof(unsigned)));
+        CK(cudaMemset(h->gepoch, 0, sizeof(unsigned)));
+      }
+    }
+    std::vector<ResidentCall> calls(n);
+    std::vector<SorC> cfs(n);
+    for (int s = 0; s < n; ++s) {
+      lesb_domain* h = hs[s];
+      cfs[s] = h->sorc();
+      calls[s] = ResidentCall{&h->g,        h->device,  h->p,        h->rhs,   &cfs[s],
+                              omega,        n_iter,     policy,      h->gxbuf, h0->gepoch,
+                              h->partials,  h->res_d,   &h->book_d->flags,     &h0->book_d->err,
+                              s > 0 ? hs[s - 1]->gxbuf : nullptr, s < n - 1 ? hs[s + 1]->gxbuf : nullptr};
+    }
+    if (!std::getenv("LESB_GROUP_SEPARATE")) {
+      CK(launch_sor_resident_group(n, calls.data(), st));
+    } else {
+      // Test form of the multi-GPU path: every slab its own cooperative launch
+      // on its own stream with its own epoch, exchanging through the
+      // neighbours' ghost slots -- as NCCL ranks do across GPUs (each launch
+      // keeps num_SMs / n tiles so the n launches can be co-resident).
+      cudaEvent_t ev_in;
+      CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev_in, st));
+      std::vector<cudaEvent_t> ev_out(n);
+      for (int s = 0; s < n; ++s) {
+        lesb_domain* h = hs[s];
+        calls[s].epoch = h->gepoch;
+        calls[s].max_tiles = resident_group_tiles(n);
+        CK(cudaStreamWaitEvent(h->st, ev_in, 0));
+        CK(launch_sor_resident(calls[s], h->st));
+        CK(cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_out[s], h->st));
+      }
+      for (int s = 0; s < n; ++s) {
+        CK(cudaStreamWaitEvent(st, ev_out[s], 0));
+        cudaEventDestroy(ev_out[s]);
+      }
+      cudaEventDestroy(ev_in);
+    }
+  }
+  // streaming passes: the colour-split layout where every slab supports it
+  bool split = !group_res && scheme == LESB_REDBLACK && h0->sor_path != 3;
+  for (int s = 0; s < n && split; ++s) split = hs[s]->split && split_supported(hs[s]->g, hs[s]->sorc());
+  if (split)
+    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, policy, st);
+  for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
+    for (int nrd = 0; nrd < 2; ++nrd) {
+      for (int s = 0; s < n; ++s) {
+        lesb_domain* h = hs[s];
+        const int nblk = split ? sor_blocks_split(h->g)
+                               : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g));
+        double* part = h->partials + ((long long)it * 2 + nrd) * nblk;
+        if (split) {
+          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, policy, part, st);
+        } else if (scheme == LESB_REDBLACK) {
+          launch_rb_pass(h->g, h->p, h->rhs, h->sorc(), omega, nrd, policy, part, st);
+        } else {
+          launch_tw_sweep(h->g, nrd == 0 ? h->p : h->pb, nrd == 0 ? h->pb : h->p, h->rhs, h->sorc(), omega, policy,
+                          part, st);
+        }
+      }
+      for (int s = 0; s < n; ++s) {
+        if (split) local_exchange_split(hs[s], nrd, st);
+        else local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
+      }
+    }
+  }
+  for (int s = 0; s < n; ++s) {
+    if (split) launch_split_unpack(hs[s]->g, hs[s]->split, hs[s]->p, policy, &hs[s]->book_d->flags, st);
+    else if (policy == 1) launch_press_halo(hs[s]->g, hs[s]->p, &hs[s]->book_d->flags, st);
+  }
+  for (int s = 0; s < n; ++s) local_exchange(hs[s], &lesb_domain::p, 1, st);
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    if (!group_res)  // (the resident solver reduces its residuals itself)
+      launch_reduce_res(h->partials,
+                        split ? sor_blocks_split(h->g)
+                              : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g)),
+                        n_iter, h->res_d, st);
+    CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  if (group_res) {  // a neighbour wait that timed out: reset the group's face buffers and report
+    unsigned e = 0;
+    CK(cudaMemcpy(&e, &h0->book_d->err, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    if (e) {
+      for (int s = 0; s < n; ++s) {
+        cudaMemset(hs[s]->gxbuf, 0, resident_xbuf_words(hs[s]->g, hs[s]->device, resident_group_tiles(n)) * 8);
+        cudaMemset(hs[s]->gepoch, 0, sizeof(unsigned));
+      }
+      cudaMemset(&h0->book_d->err, 0, sizeof(unsigned));
+      cudaDeviceSynchronize();
+      return fail(LESB_E_CUDA, "resident SOR (slab group): neighbour wait timed out");
+    }
+  }
+  return LESB_OK;
+}
+
 // One step of n in-process slabs, all enqueued on the first slab's stream:
 // each phase runs on every slab before the halo planes move.  Red-black and
 // twinned use the streaming kernels (the resident / fused solvers need the
@@ -1308,119 +1432,8 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
     if (scheme == LESB_TWINNED)
       CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
-  // Red-black on slabs of one shape: the resident solver for the whole group
-  // in one cooperative launch, tile faces crossing slab boundaries through
-  // the neighbours' ghost slots (the in-process form of the NVLink peer path)
-  bool group_res = scheme == LESB_REDBLACK && n <= resident_group_max() &&
-                   (h0->sor_path == 0 || h0->sor_path == 2) && !std::getenv("LESB_GROUP_PASSES");
-  for (int s = 0; s < n && group_res; ++s)
-    group_res = hs[s]->g.im == h0->g.im && hs[s]->g.jm == h0->g.jm && hs[s]->g.km == h0->g.km &&
-                resident_supported(hs[s]->g, hs[s]->sorc(), hs[s]->device, resident_group_tiles(n));
-  if (group_res) {
-    for (int s = 0; s < n; ++s) {
-      lesb_domain* h = hs[s];
-      if (!h->gxbuf) {
-        const size_t xb = resident_xbuf_words(h->g, h->device, resident_group_tiles(n)) * sizeof(unsigned long long);
-        CK(cudaMalloc(&h->gxbuf, xb));
-        CK(cudaMemset(h->gxbuf, 0, xb));
-        CK(cudaMalloc(&h->gepoch, sizeof(unsigned)));
-        CK(cudaMemset(h->gepoch, 0, sizeof(unsigned)));
-      }
-    }
-    std::vector<ResidentCall> calls(n);
-    std::vector<SorC> cfs(n);
-    for (int s = 0; s < n; ++s) {
-      lesb_domain* h = hs[s];
-      cfs[s] = h->sorc();
-      calls[s] = ResidentCall{&h->g,        h->device,  h->p,        h->rhs,   &cfs[s],
-                              omega,        n_iter,     1,           h->gxbuf, h0->gepoch,
-                              h->partials,  h->res_d,   &h->book_d->flags,     &h0->book_d->err,
-                              s > 0 ? hs[s - 1]->gxbuf : nullptr, s < n - 1 ? hs[s + 1]->gxbuf : nullptr};
-    }
-    if (!std::getenv("LESB_GROUP_SEPARATE")) {
-      CK(launch_sor_resident_group(n, calls.data(), st));
-    } else {
-      // Test form of the multi-GPU path: every slab its own cooperative launch
-      // on its own stream with its own epoch, exchanging through the
-      // neighbours' ghost slots -- as NCCL ranks do across GPUs (each launch
-      // keeps num_SMs / n tiles so the n launches can be co-resident).
-      cudaEvent_t ev_in;
-      CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-      CK(cudaEventRecord(ev_in, st));
-      std::vector<cudaEvent_t> ev_out(n);
-      for (int s = 0; s < n; ++s) {
-        lesb_domain* h = hs[s];
-        calls[s].epoch = h->gepoch;
-        calls[s].max_tiles = resident_group_tiles(n);
-        CK(cudaStreamWaitEvent(h->st, ev_in, 0));
-        CK(launch_sor_resident(calls[s], h->st));
-        CK(cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming));
-        CK(cudaEventRecord(ev_out[s], h->st));
-      }
-      for (int s = 0; s < n; ++s) {
-        CK(cudaStreamWaitEvent(st, ev_out[s], 0));
-        cudaEventDestroy(ev_out[s]);
-      }
-      cudaEventDestroy(ev_in);
-    }
-  }
-  // streaming passes: the colour-split layout where every slab supports it
-  bool split = !group_res && scheme == LESB_REDBLACK && h0->sor_path != 3;
-  for (int s = 0; s < n && split; ++s) split = hs[s]->split && split_supported(hs[s]->g, hs[s]->sorc());
-  if (split)
-    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, 1, st);
-  for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
-    for (int nrd = 0; nrd < 2; ++nrd) {
-      for (int s = 0; s < n; ++s) {
-        lesb_domain* h = hs[s];
-        const int nblk = split ? sor_blocks_split(h->g)
-                               : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g));
-        double* part = h->partials + ((long long)it * 2 + nrd) * nblk;
-        if (split) {
-          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, 1, part, st);
-        } else if (scheme == LESB_REDBLACK) {
-          launch_rb_pass(h->g, h->p, h->rhs, h->sorc(), omega, nrd, 1, part, st);
-        } else {
-          launch_tw_sweep(h->g, nrd == 0 ? h->p : h->pb, nrd == 0 ? h->pb : h->p, h->rhs, h->sorc(), omega, 1,
-                          part, st);
-        }
-      }
-      for (int s = 0; s < n; ++s) {
-        if (split) local_exchange_split(hs[s], nrd, st);
-        else local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
-      }
-    }
-  }
-  for (int s = 0; s < n; ++s) {
-    if (split) launch_split_unpack(hs[s]->g, hs[s]->split, hs[s]->p, 1, &hs[s]->book_d->flags, st);
-    else launch_press_halo(hs[s]->g, hs[s]->p, &hs[s]->book_d->flags, st);
-  }
-  for (int s = 0; s < n; ++s) local_exchange(hs[s], &lesb_domain::p, 1, st);
-  for (int s = 0; s < n; ++s) {
-    lesb_domain* h = hs[s];
-    if (!group_res)  // (the resident solver reduces its residuals itself)
-      launch_reduce_res(h->partials,
-                        split ? sor_blocks_split(h->g)
-                              : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g)),
-                        n_iter, h->res_d, st);
-    CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&h->book_h->flags, &h->book_d->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  }
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(st));
-  if (group_res) {  // a neighbour wait that timed out: reset the group's face buffers and report
-    unsigned e = 0;
-    CK(cudaMemcpy(&e, &h0->book_d->err, sizeof(unsigned), cudaMemcpyDeviceToHost));
-    if (e) {
-      for (int s = 0; s < n; ++s) {
-        cudaMemset(hs[s]->gxbuf, 0, resident_xbuf_words(hs[s]->g, hs[s]->device, resident_group_tiles(n)) * 8);
-        cudaMemset(hs[s]->gepoch, 0, sizeof(unsigned));
-      }
-      cudaMemset(&h0->book_d->err, 0, sizeof(unsigned));
-      cudaDeviceSynchronize();
-      return fail(LESB_E_CUDA, "resident SOR (slab group): neighbour wait timed out");
-    }
-  }
+  int rc = group_sor(hs, n, n_iter, scheme, omega, 1, st);
+  if (rc) return rc;
   unsigned bits = 0;
   for (int s = 0; s < n; ++s) {
     bits |= hs[s]->book_h->flags;
@@ -1434,6 +1447,41 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
     }
   if (fail_stage) *fail_stage = bits ? first_stage(bits) : -1;
   return bits ? LESB_NONFINITE : LESB_OK;
+}
+
+// solve_pressure (sor.py:255-309) on n in-process slabs: p and rhs are
+// the slabs' own buffers (lesb_upload of LESB_P / LESB_RHS); the residual
+// history is the sum of the slabs' histories, in slab order.
+int lesb_group_sor_solve(lesb_handle* hs, int n, int n_iter, int scheme, float omega, int halo_policy,
+                         double* residuals_out) {
+  if (!hs || n < 1) return fail(LESB_E_ARG, "bad argument");
+  if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
+  for (int s = 0; s < n; ++s) {
+    int rc = check_args_step(hs[s], n_iter, scheme);
+    if (rc) return rc;
+  }
+  lesb_domain* h0 = hs[0];
+  CK(cudaSetDevice(h0->device));
+  cudaStream_t st = h0->st;
+  for (int s = 0; s < n; ++s) {
+    lesb_domain* h = hs[s];
+    CK(cudaStreamSynchronize(h->st));
+    int rc = ensure_partials(h, n_iter);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), st));
+    if (scheme == LESB_TWINNED)
+      CK(cudaMemcpyAsync(h->pb, h->p, h->n_py * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  int rc = group_sor(hs, n, n_iter, scheme, omega, halo_policy, st);
+  if (rc) return rc;
+  for (int s = 0; s < n; ++s) hs[s]->known_finite = false;
+  if (residuals_out)
+    for (int it = 0; it < n_iter; ++it) {
+      double t = 0.0;
+      for (int s = 0; s < n; ++s) t += hs[s]->res_h[it];
+      residuals_out[it] = t;
+    }
+  return LESB_OK;
 }
 
 }  // extern "C"

@@ -18,14 +18,17 @@ from __future__ import annotations
 
 import importlib
 
+from . import cli as _cli
 from . import les as _les
 from . import sor as _sor
 
 LES_FUNCS = ("step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf", "les_viscosity",
              "strain_magnitude", "adam", "divergence", "press", "les_main")
 CLI_FUNCS = ("les_main", "run_boundary_audit")  # cli.py:23 binds les_main at import
-# cli.main dispatches through the _RUNNERS table built at import (cli.py:323-328)
-CLI_RUNNERS = {"boundary-audit": "run_boundary_audit"}
+# cli.main dispatches through the _RUNNERS table built at import (cli.py:323-328):
+# mode -> (module, function) of the device implementation
+CLI_RUNNERS = {"boundary-audit": (_les, "run_boundary_audit"), "les-standalone": (_cli, "run_les_standalone"),
+               "sor-bench": (_cli, "run_sor_bench")}
 SOR_FUNCS = ("solve_pressure", "redblack_iteration", "twinned_sweep")
 # gmcf_mini/__init__.py re-exports les_main and the solver entry points
 # (``from gmcf_mini import solve_pressure`` binds the package attribute)
@@ -62,12 +65,12 @@ def install(les_module=None, sor_module=None) -> None:
             setattr(mod, n, getattr(impl, n))
         runners = getattr(mod, "_RUNNERS", None) if names is CLI_FUNCS else None
         if isinstance(runners, dict):
-            for mode, fn in CLI_RUNNERS.items():
+            for mode, (rmod, fn) in CLI_RUNNERS.items():
                 if mode in runners:
                     key = (mod.__name__, "_RUNNERS:" + mode)
                     if key not in _saved:
                         _saved[key] = (runners, runners[mode])
-                    runners[mode] = getattr(impl, fn)
+                    runners[mode] = getattr(rmod, fn)
 
 
 def uninstall() -> None:

@@ -43,6 +43,21 @@ def write_json(path, obj) -> None:
     _atomic(Path(path), ((json.dumps(obj, indent=2) + "\n").encode(),))
 
 
+def write_sidecar(path, entries: dict) -> None:
+    """``key = value`` lines (dump.py:42-44)."""
+    lines = [f"{k} = {v}" for k, v in entries.items()]
+    _atomic(Path(path), (("\n".join(lines) + "\n").encode(),))
+
+
+def write_csv(path, header: str, rows) -> None:
+    """Comma-separated rows under a header line (dump.py:47-51): sor-bench's
+    residual histories (``iteration,residual`` with ``%.17g`` values, as the
+    device returns them) and timing tables."""
+    lines = [header]
+    lines.extend(",".join(str(c) for c in row) for row in rows)
+    _atomic(Path(path), (("\n".join(lines) + "\n").encode(),))
+
+
 def read_field(path) -> np.ndarray:
     raw = Path(path).read_bytes()
     if raw[:4] != MAGIC:

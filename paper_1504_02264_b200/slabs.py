@@ -152,6 +152,21 @@ class SlabGroup:
             raise NumericsError(N.STAGE_NAMES[stage.value], "device stage check (slabs)")
         return res
 
+    def solve(self, p0: np.ndarray, rhs: np.ndarray, omega: float, n_iter: int, scheme: Scheme = Scheme.REDBLACK,
+              halo_policy: int = 0):
+        """solve_pressure (sor.py:255-309) on the slabs: the global p0 and rhs
+        are cut into the slabs, solved together (lesb_group_sor_solve) and p
+        gathered back.  Returns (p, residuals): p bitwise equal to the
+        single-domain solve; residuals summed over the slabs in order."""
+        _check_solver_args(n_iter, scheme, 1)
+        for s in self.slabs:
+            s.upload("p", p0)
+            s.upload("rhs", rhs)
+        res = np.zeros(n_iter, np.float64)
+        N.check(N.load().lesb_group_sor_solve(self._arr, len(self.slabs), int(n_iter), _scheme_code(scheme),
+                                              float(omega), int(halo_policy), N.dptr(res)), "lesb_group_sor_solve")
+        return self.gather("p"), res
+
     def gather(self, name: str) -> np.ndarray:
         g = self.grid
         return gather([s.download(name, g.jm, g.km) for s in self.slabs], self.bounds)

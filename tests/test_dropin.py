@@ -73,10 +73,13 @@ def test_reference_pressure_halo_maps_to_press_policy(ref):
 
 def test_install_rebinds_cli_runners(ref):
     """cli.main dispatches through _RUNNERS (cli.py:323-328): install() swaps
-    the boundary-audit runner for the GPU one and uninstall() restores it."""
+    the boundary-audit, les-standalone and sor-bench runners for the GPU ones
+    and uninstall() restores them; coupled keeps the reference's runner
+    (which reaches the device through the rebound les_main)."""
     cli = pytest.importorskip("gmcf_mini.cli")
     import paper_1504_02264_b200 as P
 
+    orig_runners = dict(cli._RUNNERS)
     orig_runner = cli._RUNNERS["boundary-audit"]
     orig_fn = cli.run_boundary_audit
     orig_main = cli.les_main
@@ -85,12 +88,12 @@ def test_install_rebinds_cli_runners(ref):
         assert cli._RUNNERS["boundary-audit"] is P.les.run_boundary_audit
         assert cli.run_boundary_audit is P.les.run_boundary_audit
         assert cli.les_main is P.les.les_main
-        for mode in ("coupled", "les-standalone", "sor-bench"):
-            assert cli._RUNNERS[mode] is getattr(cli, {"coupled": "run_coupled",
-                                                       "les-standalone": "run_les_standalone",
-                                                       "sor-bench": "run_sor_bench"}[mode])
+        assert cli._RUNNERS["coupled"] is cli.run_coupled
+        assert cli._RUNNERS["les-standalone"] is P.cli.run_les_standalone
+        assert cli._RUNNERS["sor-bench"] is P.cli.run_sor_bench
     finally:
         P.uninstall()
+    assert cli._RUNNERS == orig_runners
     assert cli._RUNNERS["boundary-audit"] is orig_runner
     assert cli.run_boundary_audit is orig_fn
     assert cli.les_main is orig_main
