@@ -425,7 +425,7 @@ def run_gpu(args):
     b_solve = B_ITER * n_int * N_ITER
     achieved = b_solve / (sor_ms * 1e-3) / 1e9
     step_gbs = B_STEP * n_int / (ms_per_step * 1e-3) / 1e9
-    sor_kernel = {2: "k_sor_resident", 1: "k_sor_rbs", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(hw.h, 0)]
+    sor_kernel = {2: "k_sor_resident", 1: "k_sor_rbt", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(hw.h, 0)]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:

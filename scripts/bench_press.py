@@ -106,7 +106,7 @@ def cpu_baseline():
 print(json.dumps({
     "config": (f"press-only {im}x{jm}x{km}, " + ("RB omega 1.7" if a.scheme == "redblack" else "TW omega 1.0") +
                f", {a.n_iter} iterations, halo {a.halo}"),
-    "sor_kernel": ({1: "k_sor_rbs", 2: "k_sor_resident", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(h.h, 0)]
+    "sor_kernel": ({1: "k_sor_rbt", 2: "k_sor_resident", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(h.h, 0)]
                    if a.scheme == "redblack" else "k_sor_tw"),
     "ms_per_solve": ms, "us_per_iteration": 1000 * ms / a.n_iter,
     "mcell_iter_per_s": n * a.n_iter / (ms * 1e-3) / 1e6,
