@@ -113,6 +113,14 @@ struct lesb_domain {
   float* split = nullptr;  // colour-split p / rhs of the streaming red-black passes (4 * SplitGeo::n floats)
   void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
   int* coll_d = nullptr;      // NCCL slabs: scratch of the stage reductions
+  // x-slab streaming passes with the fused plane exchange (PassGhost):
+  // ghost planes [from west: 4 slots][from east: 4 slots] of spi words, the
+  // solve epoch, and (NCCL ranks) the neighbours' ghost buffers mapped
+  unsigned long long* ghost = nullptr;
+  unsigned* gh_epoch = nullptr;
+  void* gpeer_w = nullptr;
+  void* gpeer_e = nullptr;
+  bool ghost_ready = false;
   unsigned* repoch = nullptr;  // resident solver tag epoch
   // x-slab on NCCL ranks: the neighbour ranks' face buffers mapped through
   // CUDA IPC (peer memory over NVLink) so the resident solver exchanges tile
@@ -143,6 +151,16 @@ struct lesb_domain {
     const bool res = resident_in_use();
     ResidentBufs rb{res, device, sor_path == 3 ? 1 : 0, xbuf, repoch, &book_d->err};
     rb.split = split;
+    if (ghost_ready && !res) {  // NCCL slab on the streaming passes: exchange fused into the pass kernel
+      const long long sp = split_geo(g).spi;
+      rb.ghost.my_w = g.west_bc ? nullptr : ghost;
+      rb.ghost.my_e = g.east_bc ? nullptr : ghost + 4 * sp;
+      rb.ghost.to_w = gpeer_w ? (unsigned long long*)gpeer_w + 4 * sp : nullptr;  // the west rank's from-east planes
+      rb.ghost.to_e = gpeer_e ? (unsigned long long*)gpeer_e : nullptr;           // the east rank's from-west planes
+      rb.ghost.epoch = gh_epoch;
+      rb.ghost.err = &book_d->err;
+      rb.ghost.sys = 1;
+    }
     if (res && !(g.west_bc && g.east_bc && g.ioff == 0)) {  // x-slab: faces through the neighbours' buffers
       rb.peer_w = peer_w;
       rb.peer_e = peer_e;
@@ -200,24 +218,22 @@ void set_spacing_info(lesb_domain* h, const float* dx, const float* dy, const fl
 // streaming path) when any step fails, e.g. without peer access.
 void clear_graphs(lesb_domain* h);
 
-bool map_slab_peers(lesb_domain* h) {
-  // Every rank takes part in both collectives whatever happens locally, and
-  // the peers are used only when every rank mapped both of its neighbours:
-  // a partial mapping would leave ranks on different solver paths (with
-  // different NCCL exchange sequences).
+// Collective: every rank shares a CUDA-IPC handle of `buf` (nullptr: it
+// votes "no") with a signature, opens its west / east neighbours' buffers,
+// and keeps them only when every rank mapped both of its neighbours (an
+// all-reduce of the vote): a partial mapping would leave ranks on different
+// exchange paths.
+bool map_neighbour_bufs(lesb_domain* h, void* buf, long long sig, void** out_w, void** out_e) {
   const int nr = h->link.nranks, r = h->link.rank;
   struct Rec {
     cudaIpcMemHandle_t h;
-    long long im, jm, km, words, ok;
+    long long jm, km, sig, ok;
   } rec{};
-  // a rank without a face buffer (its slab does not fit the resident plan,
-  // or another LESB_SOR_PATH) still takes part in both collectives and
-  // votes "not mapped", so every rank keeps the streaming passes
-  rec.ok = h->xbuf != nullptr && cudaIpcGetMemHandle(&rec.h, h->xbuf) == cudaSuccess;
-  rec.im = h->g.im;
+  rec.ok = buf != nullptr && cudaIpcGetMemHandle(&rec.h, buf) == cudaSuccess;
   rec.jm = h->g.jm;
   rec.km = h->g.km;
-  rec.words = resident_xbuf_words(h->g, h->device);
+  rec.sig = sig;
+  *out_w = *out_e = nullptr;
   void* d = nullptr;
   if (cudaMalloc(&d, sizeof(Rec) * (nr + 1) + sizeof(int) * 2) != cudaSuccess) return false;
   std::vector<Rec> all(nr);
@@ -227,12 +243,11 @@ bool map_slab_peers(lesb_domain* h) {
             cudaStreamSynchronize(h->st) == cudaSuccess &&
             cudaMemcpy(all.data(), d, sizeof(Rec) * nr, cudaMemcpyDeviceToHost) == cudaSuccess;
   for (int q = 0; ok && q < nr; ++q)
-    ok = all[q].ok && all[q].im == rec.im && all[q].jm == rec.jm && all[q].km == rec.km && all[q].words == rec.words;
+    ok = all[q].ok && all[q].jm == rec.jm && all[q].km == rec.km && all[q].sig == rec.sig;
   void* w = nullptr;
   void* e = nullptr;
   if (ok && r > 0) ok = cudaIpcOpenMemHandle(&w, all[r - 1].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
   if (ok && r < nr - 1) ok = cudaIpcOpenMemHandle(&e, all[r + 1].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
-  // collective decision: min over ranks of "mapped"
   int mine = ok ? 1 : 0, every = 0;
   const bool agreed = cudaMemcpy(flag, &mine, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
                       ncclAllReduce(flag, flag + 1, 1, ncclInt, ncclMin, h->link.comm, h->st) == ncclSuccess &&
@@ -244,11 +259,30 @@ bool map_slab_peers(lesb_domain* h) {
     if (e) cudaIpcCloseMemHandle(e);
     return false;
   }
-  h->peer_w = w;
-  h->peer_e = e;
-  h->peer_ready = true;
-  clear_graphs(h);
+  *out_w = w;
+  *out_e = e;
   return true;
+}
+
+// Map the neighbours' exchange buffers of an NCCL slab at its first solve
+// (every rank takes both handshakes): the resident solver's face buffers
+// (one plan on every rank: same slab shape) and the streaming passes' ghost
+// planes.
+void map_slab_peers(lesb_domain* h) {
+  void* w = nullptr;
+  void* e = nullptr;
+  const long long rsig = h->xbuf ? resident_xbuf_words(h->g, h->device) * 1000003LL + h->g.im : -1;
+  if (map_neighbour_bufs(h, h->xbuf, rsig, &w, &e)) {
+    h->peer_w = w;
+    h->peer_e = e;
+    h->peer_ready = true;
+  }
+  if (map_neighbour_bufs(h, h->ghost, split_geo(h->g).spi, &w, &e)) {
+    h->gpeer_w = w;
+    h->gpeer_e = e;
+    h->ghost_ready = true;
+  }
+  clear_graphs(h);
 }
 
 int ensure_partials(lesb_domain* h, int n_iter) {
@@ -267,6 +301,13 @@ int ensure_partials(lesb_domain* h, int n_iter) {
     CK(cudaMemset(h->xbuf, 0, xb));
     CK(cudaMalloc(&h->repoch, sizeof(unsigned)));
     CK(cudaMemset(h->repoch, 0, sizeof(unsigned)));
+  }
+  if ((h->link.comm || h->link.west || h->link.east) && !h->ghost && split_supported(h->g, h->sorc())) {
+    const size_t gb = 8 * split_geo(h->g).spi * sizeof(unsigned long long);
+    CK(cudaMalloc(&h->ghost, gb));
+    CK(cudaMemset(h->ghost, 0, gb));
+    CK(cudaMalloc(&h->gh_epoch, sizeof(unsigned)));
+    CK(cudaMemset(h->gh_epoch, 0, sizeof(unsigned)));
   }
   if (h->link.comm && !h->peer_tried) {  // collective: every rank, whatever its own plan
     h->peer_tried = true;
@@ -649,6 +690,10 @@ int lesb_destroy(lesb_handle h) {
   if (h->gepoch) cudaFree(h->gepoch);
   if (h->split) cudaFree(h->split);
   if (h->coll_d) cudaFree(h->coll_d);
+  if (h->gpeer_w) cudaIpcCloseMemHandle(h->gpeer_w);
+  if (h->gpeer_e) cudaIpcCloseMemHandle(h->gpeer_e);
+  if (h->ghost) cudaFree(h->ghost);
+  if (h->gh_epoch) cudaFree(h->gh_epoch);
   if (h->res_d) cudaFree(h->res_d);
   if (h->book_d) cudaFree(h->book_d);
   if (h->res_h) cudaFreeHost(h->res_h);
@@ -1331,9 +1376,59 @@ static int group_sor(lesb_domain** hs, int n, int n_iter, int scheme, float omeg
   // streaming passes: the colour-split layout where every slab supports it
   bool split = !group_res && scheme == LESB_REDBLACK && h0->sor_path != 3;
   for (int s = 0; s < n && split; ++s) split = hs[s]->split && split_supported(hs[s]->g, hs[s]->sorc());
+  // the plane exchange fused into the pass kernel through the slabs' ghost
+  // planes (LESB_GHOST=0: a plane copy after every pass instead)
+  std::vector<PassGhost> gh(n);
+  bool ghosts = split && !(std::getenv("LESB_GHOST") && std::atoi(std::getenv("LESB_GHOST")) == 0);
+  for (int s = 0; s < n && ghosts; ++s) ghosts = hs[s]->ghost && ghost_supported(hs[s]->g, n_iter);
+  if (ghosts)
+    for (int s = 0; s < n; ++s) {
+      const long long sp = split_geo(hs[s]->g).spi;
+      gh[s].my_w = s > 0 ? hs[s]->ghost : nullptr;
+      gh[s].my_e = s < n - 1 ? hs[s]->ghost + 4 * sp : nullptr;
+      gh[s].to_w = s > 0 ? hs[s - 1]->ghost + 4 * sp : nullptr;
+      gh[s].to_e = s < n - 1 ? hs[s + 1]->ghost : nullptr;
+      gh[s].epoch = hs[s]->gh_epoch;
+      gh[s].err = &h0->book_d->err;
+    }
   if (split)
-    for (int s = 0; s < n; ++s) launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, policy, st);
-  for (int it = 0; it < (group_res ? 0 : n_iter); ++it) {
+    for (int s = 0; s < n; ++s) {
+      launch_split_pack(hs[s]->g, hs[s]->p, hs[s]->rhs, hs[s]->split, policy, st);
+      if (ghosts) launch_ghost_prologue(hs[s]->g, hs[s]->split, gh[s], st);
+    }
+  // With the fused exchange every slab runs its passes on its own stream,
+  // nothing ordering the slabs but the ghost tags -- what one rank per GPU
+  // does (the in-process test form of the multi-GPU path), and the slabs'
+  // half-size kernels then fill the device together (600x300x90 on two
+  // slabs: +4% over one domain, +39% serialised on one stream).
+  // LESB_GROUP_STREAMS=0 serialises them on the first slab's stream.
+  const bool sep = ghosts && !(std::getenv("LESB_GROUP_STREAMS") && std::atoi(std::getenv("LESB_GROUP_STREAMS")) == 0);
+  if (sep) {
+    cudaEvent_t ev_in;
+    CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev_in, st));
+    std::vector<cudaEvent_t> ev_out(n);
+    for (int s = 0; s < n; ++s) {
+      lesb_domain* h = hs[s];
+      CK(cudaStreamWaitEvent(h->st, ev_in, 0));
+      const int nblk = sor_blocks_split(h->g);
+      for (int it = 0; it < n_iter; ++it)
+        for (int nrd = 0; nrd < 2; ++nrd) {
+          PassGhost gp = gh[s];
+          gp.pass = 2 * it + nrd;
+          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, policy,
+                          h->partials + ((long long)it * 2 + nrd) * nblk, h->st, &gp);
+        }
+      CK(cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming));
+      CK(cudaEventRecord(ev_out[s], h->st));
+    }
+    for (int s = 0; s < n; ++s) {
+      CK(cudaStreamWaitEvent(st, ev_out[s], 0));
+      cudaEventDestroy(ev_out[s]);
+    }
+    cudaEventDestroy(ev_in);
+  }
+  for (int it = 0; it < (group_res || sep ? 0 : n_iter); ++it) {
     for (int nrd = 0; nrd < 2; ++nrd) {
       for (int s = 0; s < n; ++s) {
         lesb_domain* h = hs[s];
@@ -1341,7 +1436,9 @@ static int group_sor(lesb_domain** hs, int n, int n_iter, int scheme, float omeg
                                : (scheme == LESB_REDBLACK ? sor_blocks_rb(h->g) : sor_blocks_tw(h->g));
         double* part = h->partials + ((long long)it * 2 + nrd) * nblk;
         if (split) {
-          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, policy, part, st);
+          PassGhost gp = gh[s];
+          gp.pass = 2 * it + nrd;
+          launch_rbs_pass(h->g, h->split, h->sorc(), omega, nrd, policy, part, st, ghosts ? &gp : nullptr);
         } else if (scheme == LESB_REDBLACK) {
           launch_rb_pass(h->g, h->p, h->rhs, h->sorc(), omega, nrd, policy, part, st);
         } else {
@@ -1350,6 +1447,7 @@ static int group_sor(lesb_domain** hs, int n, int n_iter, int scheme, float omeg
         }
       }
       for (int s = 0; s < n; ++s) {
+        if (ghosts) continue;  // the pass kernels exchanged their edge planes themselves
         if (split) local_exchange_split(hs[s], nrd, st);
         else local_exchange(hs[s], (scheme == LESB_TWINNED && nrd == 0) ? &lesb_domain::pb : &lesb_domain::p, 1, st);
       }

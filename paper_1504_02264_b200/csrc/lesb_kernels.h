@@ -51,6 +51,25 @@ __device__ __forceinline__ void step_book_update(StepBook* b) {
   b->steps += 1;
 }
 
+// Streaming passes on x-slabs: the plane exchange fused into the pass
+// kernel (sor_split.cu).  Each slab keeps two ghost planes (from the west,
+// from the east) of 4 slots x SplitGeo::spi (value, tag) 64-bit words; the
+// tiles of a slab's edge planes write their new values straight into the
+// neighbour's ghost slot of the pass (peer memory over NVLink across GPUs)
+// and read their own ghost slot of the neighbour's previous pass, spinning
+// on the tag -- no copy and no collective between passes.
+struct PassGhost {
+  unsigned long long* my_w = nullptr;  // ghost planes from the west neighbour [4][spi], or nullptr (physical face)
+  unsigned long long* my_e = nullptr;  // from the east neighbour
+  unsigned long long* to_w = nullptr;  // the west neighbour's my_e (peer memory on another GPU)
+  unsigned long long* to_e = nullptr;  // the east neighbour's my_w
+  unsigned* epoch = nullptr;           // solve counter of this slab (launch_ghost_epoch), tags are unique per solve
+  unsigned* err = nullptr;             // set when a wait times out
+  int pass = 0;                        // pass of the solve (0 .. 2 n_iter - 1)
+  int sys = 0;                         // the neighbours are on other GPUs: system-scope accesses
+  bool on() const { return my_w || my_e; }
+};
+
 struct ResidentBufs {
   int use;
   int device;
@@ -65,6 +84,7 @@ struct ResidentBufs {
   StepBook* book = nullptr;
   bool* book_used = nullptr;
   float* split = nullptr;  // 4 * SplitGeo::n floats: p (colour 0, 1), rhs (colour 0, 1)
+  PassGhost ghost;         // x-slab streaming passes: fused plane exchange (ghost.on())
 };
 
 // stages.cu
@@ -114,7 +134,11 @@ bool split_supported(const Geo& g, const SorC& cf);
 int sor_blocks_split(const Geo& g);
 void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st);
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
-                     cudaStream_t st);
+                     cudaStream_t st, const PassGhost* gh = nullptr);
+// before the passes of a solve: bump the slab's epoch, then publish its
+// initial colour-1 edge planes (what the neighbours' pass 0 reads)
+void launch_ghost_prologue(const Geo& g, const float* split, const PassGhost& gh, cudaStream_t st);
+bool ghost_supported(const Geo& g, int n_iter);
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st);
 
 // sor_resident.cu

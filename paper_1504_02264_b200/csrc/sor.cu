@@ -460,18 +460,26 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
     // colour-split streaming passes: split p and rhs, 2 n_iter unit-stride
     // passes (each followed by the slab's plane exchange of the colour it
     // wrote), merge back with the final halo_fn and the press check
+    // x-slabs with mapped neighbours: the edge-plane exchange is fused into
+    // the pass kernel (PassGhost); otherwise the hook exchanges the colour's
+    // planes after every pass
     const SplitGeo sg = split_geo(g);
     const int nblk = sor_blocks_split(g);
+    const bool gho = res->ghost.on() && ghost_supported(g, n_iter);
     launch_split_pack(g, p, rhs, res->split, policy, st);
+    if (gho) launch_ghost_prologue(g, res->split, res->ghost, st);
     for (int it = 0; it < n_iter; ++it) {
       for (int c = 0; c < 2; ++c) {
-        launch_rbs_pass(g, res->split, cf, om, c, policy, partials + ((long long)it * 2 + c) * nblk, st);
-        if (hooked) hook->fn(hook->ctx, res->split + c * sg.n, sg.spi);
+        PassGhost gp = res->ghost;
+        gp.pass = 2 * it + c;
+        launch_rbs_pass(g, res->split, cf, om, c, policy, partials + ((long long)it * 2 + c) * nblk, st,
+                        gho ? &gp : nullptr);
+        if (hooked && !gho) hook->fn(hook->ctx, res->split + c * sg.n, sg.spi);
       }
     }
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
     launch_split_unpack(g, res->split, p, policy, policy == 1 ? flags : nullptr, st);
-    if (policy == 1 && hooked) hook->fn(hook->ctx, p, g.si);
+    if (hooked && (policy == 1 || gho)) hook->fn(hook->ctx, p, g.si);  // the inner x halo planes: final values
     launch_reduce_res(partials, nblk, n_iter, res_dev, st);
     return cudaGetLastError();
   }

@@ -299,6 +299,68 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ float4 lds4(const float* a) { return *reinterpret_cast<const float4*>(a); }
 
+// ---- fused plane exchange of x-slabs (PassGhost) ----
+// tag of pass p (-1: the state before the first pass) in solve `epoch`
+__device__ __forceinline__ unsigned ghost_tag(unsigned epoch, int p) {
+  return (epoch << 12) | (unsigned)((p + 1) & 0xfff);
+}
+__device__ __forceinline__ void gld2(const unsigned long long* a, bool sys, unsigned long long& x,
+                                     unsigned long long& y) {
+  if (sys) asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a));
+  else asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a));
+}
+__device__ __forceinline__ void gst2(unsigned long long* a, bool sys, unsigned long long x, unsigned long long y) {
+  if (sys) asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(a), "l"(x), "l"(y) : "memory");
+  else asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(a), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ unsigned long long gword(float v, unsigned tag) {
+  return ((unsigned long long)tag << 32) | __float_as_uint(v);
+}
+// four ghost words of the neighbour's pass: spin until every tag is the
+// expected one (each word is written with one single-copy-atomic 64-bit
+// store, so a matching tag carries its value); a wait longer than ~2 s
+// sets *err and returns what it has (the host reports the timeout)
+__device__ __forceinline__ float4 ghost_ld4(const unsigned long long* a, unsigned tag, bool sys, unsigned* err) {
+  unsigned long long w0, w1, w2, w3;
+  gld2(a, sys, w0, w1);
+  gld2(a + 2, sys, w2, w3);
+  if ((unsigned)(w0 >> 32) != tag || (unsigned)(w1 >> 32) != tag || (unsigned)(w2 >> 32) != tag ||
+      (unsigned)(w3 >> 32) != tag) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((unsigned)(w0 >> 32) != tag || (unsigned)(w1 >> 32) != tag || (unsigned)(w2 >> 32) != tag ||
+           (unsigned)(w3 >> 32) != tag) {
+      __nanosleep(64);
+      gld2(a, sys, w0, w1);
+      gld2(a + 2, sys, w2, w3);
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 2000000000ull) {
+        atomicExch(err, 1u);
+        break;
+      }
+    }
+  }
+  return make_float4(__uint_as_float((unsigned)w0), __uint_as_float((unsigned)w1), __uint_as_float((unsigned)w2),
+                     __uint_as_float((unsigned)w3));
+}
+__device__ __forceinline__ void ghost_st4(unsigned long long* a, const float (&v)[4], unsigned tag, bool sys) {
+  gst2(a, sys, gword(v[0], tag), gword(v[1], tag));
+  gst2(a + 2, sys, gword(v[2], tag), gword(v[3], tag));
+}
+
+// the per-tile ghost pointers of a thread: its first row's words in this
+// pass's slots (nullptr where the tile has no such exchange)
+struct TileGhost {
+  const unsigned long long* rw;  // read W: my_w, slot of pass p-1
+  const unsigned long long* re;  // read E: my_e, slot of pass p-1
+  unsigned long long* pw;        // publish to the west neighbour (its my_e), slot of pass p
+  unsigned long long* pe;        // publish to the east neighbour (its my_w), slot of pass p
+  unsigned rtag, wtag;
+  bool sys;
+  unsigned* err;
+};
+
 struct RbtPlan {
   int rpt;     // rows per thread per tile (even)
   int tr;      // rows per tile
@@ -319,7 +381,7 @@ template <int POL, int S0, int RPT>
 __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plane, int khp, int spi, float* own_g,
                                          float* oth_g, const SorC& cf, float om, const bool (&in0)[4],
                                          const bool (&in1)[4], bool lead, int i, int j, int o, int sro, int nr,
-                                         double& acc) {
+                                         double& acc, const TileGhost& tg) {
   const float* s_own = st + sro;
   const float* s_rhs = s_own + plane;
   const float* s_e = s_own + 2 * plane;
@@ -330,7 +392,10 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
   for (int h = 0; h < RPT; ++h) {
     if (h >= nr) break;
     const int ro = h * khp;
-    const float4 C = lds4(s_own + ro), RH = lds4(s_rhs + ro), E = lds4(s_e + ro), W = lds4(s_w + ro);
+    const float4 C = lds4(s_own + ro), RH = lds4(s_rhs + ro);
+    // x neighbours: staged, or (slab edge planes) the neighbour's words of its previous pass
+    const float4 E = tg.re ? ghost_ld4(tg.re + ro, tg.rtag, tg.sys, tg.err) : lds4(s_e + ro);
+    const float4 W = tg.rw ? ghost_ld4(tg.rw + ro, tg.rtag, tg.sys, tg.err) : lds4(s_w + ro);
     const float4 So = lds4(s_mid + ro - khp), M = lds4(s_mid + ro), N = lds4(s_mid + ro + khp);
     float val[4];
     const int go = o + ro;
@@ -341,6 +406,8 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
       if (POL != 0 && lead) oth_g[go] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
     }
     st4(own_g + go, val[0], val[1], val[2], val[3]);
+    if (tg.pw) ghost_st4(tg.pw + ro, val, tg.wtag, tg.sys);  // straight into the neighbours' ghost planes
+    if (tg.pe) ghost_st4(tg.pe + ro, val, tg.wtag, tg.sys);
     if (wmir) st4(oth_g + go - spi, val[0], val[1], val[2], val[3]);  // W mirror: p[0,j,k] = p[1,j,k]
     if (POL == 1) {  // even jm: p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k] (same colour)
       if (j + h == 1) st4(own_g + go + g.jm * khp, val[0], val[1], val[2], val[3]);
@@ -352,7 +419,7 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
 template <int POL, int RPT>
 __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __restrict__ ps,
                                                  const float* __restrict__ rs, SorC cf, float om, int c, RbtPlan pl,
-                                                 double* __restrict__ partials) {
+                                                 double* __restrict__ partials, PassGhost gh) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
   float* stages = reinterpret_cast<float*>(smem_raw + 128);
@@ -369,24 +436,39 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // tile t (plane-major): plane 1 + t / ntj, rows from 1 + (t % ntj) * tr;
-  // the CTA walks t = blockIdx.x + k * gridDim.x with incremental (i, jt)
+  // tile t (plane-major): plane position t / ntj, rows from 1 + (t % ntj) * tr;
+  // the CTA walks t = blockIdx.x + k * gridDim.x with incremental (pos, jt).
+  // With the fused slab exchange the edge planes go first (position 0: plane
+  // 1, position 1: plane im), so their words reach the neighbours early.
   const int di = (int)gridDim.x / pl.ntj, djt = (int)gridDim.x % pl.ntj;
-  auto issue = [&](int i, int jt, int s) {
+  const bool ghosts = gh.my_w || gh.my_e;
+  auto plane_of = [&](int pos) {
+    if (!ghosts) return 1 + pos;
+    return pos == 0 ? 1 : (pos == 1 ? g.im : pos);
+  };
+  auto issue = [&](int pos, int jt, int s) {
+    const int i = plane_of(pos);
     const int j0 = 1 + jt * pl.tr;
     const int nrow = min(pl.tr, g.jm - j0 + 1);
     const unsigned rb = (unsigned)(nrow * khp * 4);
     float* st = stages + s * sfl;
     const int go = i * spi + j0 * khp;
-    mbar_expect_tx(&bar[s], 4 * rb + rb + 2u * khp * 4);
+    const bool skip_e = gh.my_e && i == g.im, skip_w = gh.my_w && i == 1;  // from the ghost planes instead
+    mbar_expect_tx(&bar[s], (skip_e ? 0u : rb) + (skip_w ? 0u : rb) + 2 * rb + rb + 2u * khp * 4);
     bulk_g2s(st, own_g + go, rb, &bar[s]);
     bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
-    bulk_g2s(st + 2 * plane, oth_g + go + spi, rb, &bar[s]);
-    bulk_g2s(st + 3 * plane, oth_g + go - spi, rb, &bar[s]);
+    if (!skip_e) bulk_g2s(st + 2 * plane, oth_g + go + spi, rb, &bar[s]);
+    if (!skip_w) bulk_g2s(st + 3 * plane, oth_g + go - spi, rb, &bar[s]);
     bulk_g2s(st + 4 * plane, oth_g + go - khp, rb + 2u * khp * 4, &bar[s]);
   };
+  unsigned rtag = 0, wtag = 0;
+  if (ghosts) {
+    const unsigned ep = *(volatile const unsigned*)gh.epoch;
+    rtag = ghost_tag(ep, gh.pass - 1);
+    wtag = ghost_tag(ep, gh.pass);
+  }
   const int my = (pl.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
-  int ii = 1 + (int)blockIdx.x / pl.ntj, jt = (int)blockIdx.x % pl.ntj;  // tile k of the compute loop
+  int ii = (int)blockIdx.x / pl.ntj, jt = (int)blockIdx.x % pl.ntj;  // tile k of the compute loop (position, rows)
   if (tid == 0) {
     int pi = ii, pj = jt;
     for (int k = 0; k < pl.ns && k < my; ++k) {
@@ -421,12 +503,24 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
     const int j = 1 + jt * pl.tr + r0;
     const int nr = g.jm - j + 1;  // rows left in the plane from the thread's first row
     if (nr > 0) {
-      const int o = ii * spi + j * khp + 4 * q;
+      const int pi = plane_of(ii);
+      const int o = pi * spi + j * khp + 4 * q;
       const float* st = stages + s * sfl;
-      if (((c + ii + g.ioff) & 1) == 0)
-        rbt_rows<POL, 0, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, ii, j, o, sro, nr, acc);
+      TileGhost tg{nullptr, nullptr, nullptr, nullptr, rtag, wtag, gh.sys != 0, gh.err};
+      if (ghosts) {
+        const int go = j * khp + 4 * q;  // the thread's word offset inside a ghost plane slot
+        const int rs_ = ((gh.pass - 1) & 3) * spi + go, ws_ = (gh.pass & 3) * spi + go;
+        if (pi == 1 && gh.my_w) tg.rw = gh.my_w + rs_;
+        if (pi == g.im && gh.my_e) tg.re = gh.my_e + rs_;
+        if (pi == 1 && gh.to_w) tg.pw = gh.to_w + ws_;
+        if (pi == g.im && gh.to_e) tg.pe = gh.to_e + ws_;
+      }
+      if (((c + pi + g.ioff) & 1) == 0)
+        rbt_rows<POL, 0, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
+                              tg);
       else
-        rbt_rows<POL, 1, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, ii, j, o, sro, nr, acc);
+        rbt_rows<POL, 1, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
+                              tg);
     }
     __syncthreads();  // every thread is done with stage s
     if (tid == 0 && k + pl.ns < my) {
@@ -569,6 +663,38 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
 
 static bool rbt_ok(const SplitGeo& sg) { return sg.kh4 <= 512 && !use_reg_kernel(); }
 
+bool ghost_supported(const Geo& g, int n_iter) { return rbt_ok(split_geo(g)) && 2 * n_iter <= 4094; }
+
+// bump the solve epoch, then publish the slab's initial colour-1 edge-plane
+// values (tag of pass -1, slot 3) into the neighbours' ghost planes
+__global__ void k_ghost_epoch(unsigned* epoch) {
+  if (threadIdx.x == 0) *epoch += 1;
+}
+__global__ void k_ghost_publish0(Geo g, SplitGeo sg, const float* __restrict__ ps, PassGhost gh) {
+  const unsigned tag = ghost_tag(*(volatile const unsigned*)gh.epoch, -1);
+  const float* c1 = ps + sg.n;  // colour 1
+  const int spi = (int)sg.spi;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < spi; w += gridDim.x * blockDim.x) {
+    const unsigned long long slot = 3ull * spi + w;
+    if (gh.to_w) {
+      const unsigned long long v = gword(c1[spi + w], tag);  // plane 1
+      if (gh.sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(gh.to_w + slot), "l"(v) : "memory");
+      else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(gh.to_w + slot), "l"(v) : "memory");
+    }
+    if (gh.to_e) {
+      const unsigned long long v = gword(c1[(long long)g.im * spi + w], tag);  // plane im
+      if (gh.sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(gh.to_e + slot), "l"(v) : "memory");
+      else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(gh.to_e + slot), "l"(v) : "memory");
+    }
+  }
+}
+
+void launch_ghost_prologue(const Geo& g, const float* split, const PassGhost& gh, cudaStream_t st) {
+  k_ghost_epoch<<<1, 32, 0, st>>>(gh.epoch);
+  const SplitGeo sg = split_geo(g);
+  k_ghost_publish0<<<(unsigned)std::min<long long>(148, (sg.spi + 255) / 256), 256, 0, st>>>(g, sg, split, gh);
+}
+
 int sor_blocks_split(const Geo& g) {  // residual partials per pass: one per warp
   const SplitGeo sg = split_geo(g);
   if (rbt_ok(sg)) {
@@ -581,7 +707,8 @@ int sor_blocks_split(const Geo& g) {  // residual partials per pass: one per war
 }
 
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
-                     cudaStream_t st) {
+                     cudaStream_t st, const PassGhost* ghp) {
+  const PassGhost gh = ghp ? *ghp : PassGhost{};
   const SplitGeo sg = split_geo(g);
   float* rs = split + 2 * sg.n;
   const int pol = policy == 1 ? ((g.jm & 1) ? 2 : 1) : 0;
@@ -591,13 +718,13 @@ void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c
     const RbtPlan pl = rbt_plan(g, sg);
     const dim3 block(sg.kh4, pl.tr / pl.rpt);
     if (pl.rpt == 4) {
-      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
-      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
-      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
     } else {
-      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
-      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
-      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials);
+      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
     }
     return;
   }

@@ -30,7 +30,7 @@ def single(P, st, inflow, n_steps, n_iter, scheme):
     return out
 
 
-@pytest.mark.parametrize("solver", ["resident", "separate", "passes"])
+@pytest.mark.parametrize("solver", ["resident", "separate", "passes", "passes-copies", "passes-serial"])
 @pytest.mark.parametrize("dims,nslabs,scheme", [
     ((24, 10, 8), 2, "redblack"),
     ((24, 10, 8), 3, "redblack"),
@@ -46,14 +46,24 @@ def test_slabs_equal_single_domain(dims, nslabs, scheme, solver, monkeypatch):
     in-process form of the NVLink peer path); LESB_GROUP_SEPARATE launches
     every slab on its own stream with its own epoch (what each rank does on
     its own GPU); LESB_GROUP_PASSES forces the streaming colour passes with
-    plane copies."""
+    plane copies -- by default with the exchange fused into the pass kernel
+    (edge-plane values written straight into the neighbour's ghost planes,
+    tag-checked) and every slab's passes on its own stream ordered only by
+    the ghost tags (the multi-GPU protocol); "-serial" with the slabs'
+    passes on one stream, "-copies" with a plane copy after every pass."""
     import paper_1504_02264_b200 as P
     from paper_1504_02264_b200.slabs import SlabGroup
 
     monkeypatch.delenv("LESB_GROUP_PASSES", raising=False)
     monkeypatch.delenv("LESB_GROUP_SEPARATE", raising=False)
-    if solver == "passes":
+    monkeypatch.delenv("LESB_GHOST", raising=False)
+    monkeypatch.delenv("LESB_GROUP_STREAMS", raising=False)
+    if solver.startswith("passes"):
         monkeypatch.setenv("LESB_GROUP_PASSES", "1")
+        if solver == "passes-copies":
+            monkeypatch.setenv("LESB_GHOST", "0")
+        elif solver == "passes-serial":
+            monkeypatch.setenv("LESB_GROUP_STREAMS", "0")
     elif solver == "separate":  # one launch per slab, own stream and epoch: the per-GPU form
         monkeypatch.setenv("LESB_GROUP_SEPARATE", "1")
     P.runtime.set_sor_path(0)
