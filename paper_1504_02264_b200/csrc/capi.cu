@@ -286,8 +286,9 @@ void map_slab_peers(lesb_domain* h) {
 }
 
 int ensure_partials(lesb_domain* h, int n_iter) {
-  const int maxblk = std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)),
-                              std::max(resident_partials(h->g, h->device), sor_blocks_split(h->g)));
+  int maxblk = std::max(std::max(sor_blocks_rb(h->g), sor_blocks_tw(h->g)),
+                        std::max(resident_partials(h->g, h->device), sor_blocks_split(h->g)));
+  if (tws_supported(h->g, h->sorc())) maxblk = std::max(maxblk, sor_blocks_tws(h->g));
   long long need = (long long)n_iter * 2 * maxblk + reduce_scratch(maxblk, n_iter);
   if (need > h->partials_cap) {
     if (h->partials) cudaFree(h->partials);
@@ -314,7 +315,7 @@ int ensure_partials(lesb_domain* h, int n_iter) {
     map_slab_peers(h);  // on failure the slab keeps the streaming colour passes
   }
   if (!h->split && h->sor_path != 3 && !h->resident_in_use() && split_supported(h->g, h->sorc())) {
-    const size_t sb = 4 * split_geo(h->g).n * sizeof(float);
+    const size_t sb = 6 * split_geo(h->g).n * sizeof(float);
     CK(cudaMalloc(&h->split, sb));
     CK(cudaMemset(h->split, 0, sb));
   }

@@ -83,7 +83,7 @@ struct ResidentBufs {
   // the end-of-step bookkeeping (*book_used is set when it took it over)
   StepBook* book = nullptr;
   bool* book_used = nullptr;
-  float* split = nullptr;  // 4 * SplitGeo::n floats: p (colour 0, 1), rhs (colour 0, 1)
+  float* split = nullptr;  // 6 * SplitGeo::n floats: p (colour 0, 1), rhs (colour 0, 1), p' (twinned ping-pong)
   PassGhost ghost;         // x-slab streaming passes: fused plane exchange (ghost.on())
 };
 
@@ -132,13 +132,20 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
 SplitGeo split_geo(const Geo& g);
 bool split_supported(const Geo& g, const SorC& cf);
 int sor_blocks_split(const Geo& g);
-void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st);
+// p_copy: a second destination of the split p (the twinned sweeps' second buffer)
+void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st,
+                       float* p_copy = nullptr);
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
                      cudaStream_t st, const PassGhost* gh = nullptr);
 // before the passes of a solve: bump the slab's epoch, then publish its
 // initial colour-1 edge planes (what the neighbours' pass 0 reads)
 void launch_ghost_prologue(const Geo& g, const float* split, const PassGhost& gh, cudaStream_t st);
 bool ghost_supported(const Geo& g, int n_iter);
+// twinned sweeps on the colour-split layout (single domains): src -> dst, both colours
+bool tws_supported(const Geo& g, const SorC& cf);
+int sor_blocks_tws(const Geo& g);
+void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* rhs_split, const SorC& cf, float om,
+                      int policy, double* partials, cudaStream_t st);
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st);
 
 // sor_resident.cu

@@ -432,6 +432,8 @@ int sor_kernels_per_solve(const Geo& g, const SorC& cf, int n_iter, int scheme, 
   const int red = (int)(reduce_scratch(scheme == 0 ? sor_blocks_rb(g) : sor_blocks_tw(g), n_iter) > 0) + 1;
   if (scheme == 0 && !natural && split_supported(g, cf))  // pack, passes (+ y snapshots), unpack, reduction
     return 1 + (oddy ? 4 : 2) * n_iter + 1 + ((int)(reduce_scratch(sor_blocks_split(g), n_iter) > 0) + 1);
+  if (scheme == 1 && !natural && tws_supported(g, cf))  // pack, 2 sweeps per iteration, unpack, reduction
+    return 1 + 2 * n_iter + 1 + ((int)(reduce_scratch(sor_blocks_tws(g), n_iter) > 0) + 1);
   int per_iter = 2;
   if (scheme == 0 && oddy) per_iter = 4;
   return per_iter * n_iter + (policy == 1 ? 1 : 0) + red;
@@ -480,6 +482,25 @@ cudaError_t enqueue_sor(const Geo& g, float* p, float* pb, const float* rhs, con
     if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
     launch_split_unpack(g, res->split, p, policy, policy == 1 ? flags : nullptr, st);
     if (hooked && (policy == 1 || gho)) hook->fn(hook->ctx, p, g.si);  // the inner x halo planes: final values
+    launch_reduce_res(partials, nblk, n_iter, res_dev, st);
+    return cudaGetLastError();
+  }
+  if (scheme == 1 && res && res->split && !res->natural && !hooked && tws_supported(g, cf)) {
+    // twinned sweeps on the colour-split layout: pack p into both buffers
+    // (the stored / closed-form halos live in both), sweep A -> B -> A, the
+    // newest iterate ends in A (component 0, sor.py:308-309)
+    const SplitGeo sg = split_geo(g);
+    float* A = res->split;
+    float* B = res->split + 4 * sg.n;
+    const float* R = res->split + 2 * sg.n;
+    const int nblk = sor_blocks_tws(g);
+    launch_split_pack(g, p, rhs, res->split, policy, st, B);
+    for (int it = 0; it < n_iter; ++it) {
+      launch_tws_sweep(g, A, B, R, cf, om, policy, partials + ((long long)it * 2 + 0) * nblk, st);
+      launch_tws_sweep(g, B, A, R, cf, om, policy, partials + ((long long)it * 2 + 1) * nblk, st);
+    }
+    if (marks && marks->after_passes) cudaEventRecordWithFlags(marks->after_passes, st, cudaEventRecordExternal);
+    launch_split_unpack(g, A, p, policy, policy == 1 ? flags : nullptr, st);
     launch_reduce_res(partials, nblk, n_iter, res_dev, st);
     return cudaGetLastError();
   }

@@ -100,7 +100,7 @@ inline void rbs_shape(const SplitGeo& s, int* bx, int* by) {
 template <int POL>
 __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const float* __restrict__ p,
                                                     const float* __restrict__ rhs, float* __restrict__ ps,
-                                                    float* __restrict__ rs) {
+                                                    float* __restrict__ rs, float* __restrict__ ps2) {
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= nrow) return;
@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const fl
     const long long d = c * sg.n + rb + (k >> 1);
     ps[d] = val;
     rs[d] = src_r[k];
+    if (ps2) ps2[d] = val;
   }
 }
 
@@ -381,7 +382,7 @@ template <int POL, int S0, int RPT>
 __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plane, int khp, int spi, float* own_g,
                                          float* oth_g, const SorC& cf, float om, const bool (&in0)[4],
                                          const bool (&in1)[4], bool lead, int i, int j, int o, int sro, int nr,
-                                         double& acc, const TileGhost& tg) {
+                                         double& acc, const TileGhost& tg, bool twin) {
   const float* s_own = st + sro;
   const float* s_rhs = s_own + plane;
   const float* s_e = s_own + 2 * plane;
@@ -405,21 +406,38 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
       rbs_row<1>(cf, om, C, RH, E, W, N, So, M, s_mid[ro + 4], in1, val, acc);
       if (POL != 0 && lead) oth_g[go] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
     }
-    st4(own_g + go, val[0], val[1], val[2], val[3]);
+    if (twin && POL != 0 && lead && ((S0 + h) & 1) == 0) {
+      // twinned sweep: slot 0 of this row is the k = 0 halo cell, which the
+      // other colour's tile of this launch sets (its B mirror): leave it
+      own_g[go + 1] = val[1];
+      own_g[go + 2] = val[2];
+      own_g[go + 3] = val[3];
+    } else {
+      st4(own_g + go, val[0], val[1], val[2], val[3]);
+    }
     if (tg.pw) ghost_st4(tg.pw + ro, val, tg.wtag, tg.sys);  // straight into the neighbours' ghost planes
     if (tg.pe) ghost_st4(tg.pe + ro, val, tg.wtag, tg.sys);
     if (wmir) st4(oth_g + go - spi, val[0], val[1], val[2], val[3]);  // W mirror: p[0,j,k] = p[1,j,k]
-    if (POL == 1) {  // even jm: p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k] (same colour)
-      if (j + h == 1) st4(own_g + go + g.jm * khp, val[0], val[1], val[2], val[3]);
-      if (j + h == g.jm) st4(own_g + go - g.jm * khp, val[0], val[1], val[2], val[3]);
+    if (POL == 1 || POL == 3) {  // p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k]
+      // even jm: the same colour (own array); odd jm (twinned only, POL 3:
+      // the sweep never reads what it writes): the other colour's array
+      float* yt = POL == 1 ? own_g : oth_g;
+      if (j + h == 1) st4(yt + go + g.jm * khp, val[0], val[1], val[2], val[3]);
+      if (j + h == g.jm) st4(yt + go - g.jm * khp, val[0], val[1], val[2], val[3]);
     }
   }
 }
 
+// One colour pass (c >= 0: red-black, in place: src == dst) or one twinned
+// (Jacobi) sweep over both colours (c < 0: src -> dst, both colours' tiles
+// interleaved per plane row chunk so they share their loads in L2).
+// POL 0: stored halo; 1: press, even jm (y mirrors into the same colour);
+// 2: press, odd jm, red-black (y halo rows refreshed before the pass);
+// 3: press, odd jm, twinned (y mirrors into the other colour of dst).
 template <int POL, int RPT>
-__global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __restrict__ ps,
-                                                 const float* __restrict__ rs, SorC cf, float om, int c, RbtPlan pl,
-                                                 double* __restrict__ partials, PassGhost gh) {
+__global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float* src, float* dst,
+                                                 const float* __restrict__ rs, SorC cf, float om, int c_fixed,
+                                                 RbtPlan pl, double* __restrict__ partials, PassGhost gh) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem_raw);
   float* stages = reinterpret_cast<float*>(smem_raw + 128);
@@ -427,9 +445,7 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
   const int spi = (int)sg.spi;
   const int plane = pl.tr * khp;
   const int sfl = (5 * pl.tr + 2) * khp;
-  float* own_g = ps + (long long)c * sg.n;
-  float* oth_g = ps + (long long)(c ^ 1) * sg.n;
-  const float* rhs_g = rs + (long long)c * sg.n;
+  const int ncol = c_fixed < 0 ? 2 : 1;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   if (tid == 0) {
     for (int s = 0; s < pl.ns; ++s) mbar_init(&bar[s], 1);
@@ -440,26 +456,37 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
   // the CTA walks t = blockIdx.x + k * gridDim.x with incremental (pos, jt).
   // With the fused slab exchange the edge planes go first (position 0: plane
   // 1, position 1: plane im), so their words reach the neighbours early.
-  const int di = (int)gridDim.x / pl.ntj, djt = (int)gridDim.x % pl.ntj;
   const bool ghosts = gh.my_w || gh.my_e;
   auto plane_of = [&](int pos) {
     if (!ghosts) return 1 + pos;
     return pos == 0 ? 1 : (pos == 1 ? g.im : pos);
   };
-  auto issue = [&](int pos, int jt, int s) {
+  // tile t -> (plane position, row chunk, colour)
+  auto decode = [&](int t, int& pos, int& jt, int& c) {
+    const int r = ncol == 2 ? (t >> 1) : t;
+    c = ncol == 2 ? (t & 1) : c_fixed;
+    pos = r / pl.ntj;
+    jt = r - pos * pl.ntj;
+  };
+  auto issue = [&](int t, int s) {
+    int pos, jt, c;
+    decode(t, pos, jt, c);
     const int i = plane_of(pos);
     const int j0 = 1 + jt * pl.tr;
     const int nrow = min(pl.tr, g.jm - j0 + 1);
     const unsigned rb = (unsigned)(nrow * khp * 4);
     float* st = stages + s * sfl;
     const int go = i * spi + j0 * khp;
+    const float* own_s = src + (long long)c * sg.n;
+    const float* oth_s = src + (long long)(c ^ 1) * sg.n;
+    const float* rhs_g = rs + (long long)c * sg.n;
     const bool skip_e = gh.my_e && i == g.im, skip_w = gh.my_w && i == 1;  // from the ghost planes instead
     mbar_expect_tx(&bar[s], (skip_e ? 0u : rb) + (skip_w ? 0u : rb) + 2 * rb + rb + 2u * khp * 4);
-    bulk_g2s(st, own_g + go, rb, &bar[s]);
+    bulk_g2s(st, own_s + go, rb, &bar[s]);
     bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
-    if (!skip_e) bulk_g2s(st + 2 * plane, oth_g + go + spi, rb, &bar[s]);
-    if (!skip_w) bulk_g2s(st + 3 * plane, oth_g + go - spi, rb, &bar[s]);
-    bulk_g2s(st + 4 * plane, oth_g + go - khp, rb + 2u * khp * 4, &bar[s]);
+    if (!skip_e) bulk_g2s(st + 2 * plane, oth_s + go + spi, rb, &bar[s]);
+    if (!skip_w) bulk_g2s(st + 3 * plane, oth_s + go - spi, rb, &bar[s]);
+    bulk_g2s(st + 4 * plane, oth_s + go - khp, rb + 2u * khp * 4, &bar[s]);
   };
   unsigned rtag = 0, wtag = 0;
   if (ghosts) {
@@ -467,24 +494,9 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
     rtag = ghost_tag(ep, gh.pass - 1);
     wtag = ghost_tag(ep, gh.pass);
   }
-  const int my = (pl.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
-  int ii = (int)blockIdx.x / pl.ntj, jt = (int)blockIdx.x % pl.ntj;  // tile k of the compute loop (position, rows)
-  if (tid == 0) {
-    int pi = ii, pj = jt;
-    for (int k = 0; k < pl.ns && k < my; ++k) {
-      issue(pi, pj, k);
-      pi += di;
-      pj += djt;
-      if (pj >= pl.ntj) { pj -= pl.ntj; ++pi; }
-    }
-  }
-  // the issue cursor runs ns tiles ahead of the compute cursor
-  int ni = ii, nj = jt;
-  for (int k = 0; k < pl.ns; ++k) {
-    ni += di;
-    nj += djt;
-    if (nj >= pl.ntj) { nj -= pl.ntj; ++ni; }
-  }
+  const int my = (pl.ntiles * ncol - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
+  if (tid == 0)
+    for (int k = 0; k < pl.ns && k < my; ++k) issue((int)blockIdx.x + k * (int)gridDim.x, k);
   // per-thread invariants: its slot group q, its rows r0 .. r0+RPT-1 of a tile
   const int q = threadIdx.x, r0 = RPT * threadIdx.y;
   bool in0[4], in1[4];
@@ -499,6 +511,10 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
   double acc = 0.0;
   for (int k = 0; k < my; ++k) {
     const int s = k % pl.ns;
+    int ii, jt, c;
+    decode((int)blockIdx.x + k * (int)gridDim.x, ii, jt, c);
+    float* own_g = dst + (long long)c * sg.n;
+    float* oth_g = dst + (long long)(c ^ 1) * sg.n;
     mbar_wait(&bar[s], (unsigned)((k / pl.ns) & 1));
     const int j = 1 + jt * pl.tr + r0;
     const int nr = g.jm - j + 1;  // rows left in the plane from the thread's first row
@@ -517,22 +533,16 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, float* __re
       }
       if (((c + pi + g.ioff) & 1) == 0)
         rbt_rows<POL, 0, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
-                              tg);
+                              tg, ncol == 2);
       else
         rbt_rows<POL, 1, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
-                              tg);
+                              tg, ncol == 2);
     }
     __syncthreads();  // every thread is done with stage s
     if (tid == 0 && k + pl.ns < my) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async overwrite
-      issue(ni, nj, s);
+      issue((int)blockIdx.x + (k + pl.ns) * (int)gridDim.x, s);
     }
-    ii += di;
-    jt += djt;
-    if (jt >= pl.ntj) { jt -= pl.ntj; ++ii; }
-    ni += di;
-    nj += djt;
-    if (nj >= pl.ntj) { nj -= pl.ntj; ++ni; }
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((tid & 31) == 0) {
@@ -594,12 +604,13 @@ __global__ void __launch_bounds__(256) k_split_unpack(Geo g, SplitGeo sg, const 
 
 }  // namespace
 
-void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st) {
+void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st,
+                       float* p_copy) {
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
   const unsigned nb = (unsigned)((nrow + 7) / 8);
-  if (policy == 1) k_split_pack<1><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n);
-  else k_split_pack<0><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n);
+  if (policy == 1) k_split_pack<1><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+  else k_split_pack<0><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
 }
 
 static dim3 rbs_grid(const Geo& g, const SplitGeo& sg, int* bx, int* by) {
@@ -652,6 +663,7 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
     cudaFuncSetAttribute(k_sor_rbt<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sor_rbt<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sor_rbt<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sor_rbt<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   if (rpt == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 4>, pl.threads, pl.smem);
@@ -709,6 +721,7 @@ int sor_blocks_split(const Geo& g) {  // residual partials per pass: one per war
 void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c, int policy, double* partials,
                      cudaStream_t st, const PassGhost* ghp) {
   const PassGhost gh = ghp ? *ghp : PassGhost{};
+  float* ps = split;
   const SplitGeo sg = split_geo(g);
   float* rs = split + 2 * sg.n;
   const int pol = policy == 1 ? ((g.jm & 1) ? 2 : 1) : 0;
@@ -718,13 +731,13 @@ void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c
     const RbtPlan pl = rbt_plan(g, sg);
     const dim3 block(sg.kh4, pl.tr / pl.rpt);
     if (pl.rpt == 4) {
-      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
-      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
-      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
     } else {
-      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
-      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
-      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, split, rs, cf, om, c, pl, partials, gh);
+      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
     }
     return;
   }
@@ -734,6 +747,37 @@ void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c
   if (pol == 2) k_sor_rbs<2><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
   else if (pol == 1) k_sor_rbs<1><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
   else k_sor_rbs<0><<<grid, block, 0, st>>>(g, sg, split, rs, cf, om, c, partials);
+}
+
+bool tws_supported(const Geo& g, const SorC& cf) { return split_supported(g, cf) && rbt_ok(split_geo(g)); }
+
+int sor_blocks_tws(const Geo& g) {  // residual partials per sweep: one per warp of the persistent grid
+  const SplitGeo sg = split_geo(g);
+  const RbtPlan pl = rbt_plan(g, sg);
+  return pl.grid * ((pl.threads + 31) / 32);
+}
+
+// One twinned (Jacobi) sweep (sor.py:206-246) on the colour-split layout:
+// src (both colours) -> dst (both colours), the halo of the press policy
+// kept in dst by the same mirror writes as the red-black pass (the
+// reference applies halo_fn to the new component after every sweep,
+// sor.py:292-307).
+void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* rhs_split, const SorC& cf, float om,
+                      int policy, double* partials, cudaStream_t st) {
+  const SplitGeo sg = split_geo(g);
+  const RbtPlan pl = rbt_plan(g, sg);
+  const dim3 block(sg.kh4, pl.tr / pl.rpt);
+  const PassGhost gh{};
+  const int pol = policy == 1 ? ((g.jm & 1) ? 3 : 1) : 0;
+  if (pl.rpt == 4) {
+    if (pol == 3) k_sor_rbt<3, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+    else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+    else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+  } else {
+    if (pol == 3) k_sor_rbt<3, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+    else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+    else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
+  }
 }
 
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st) {

@@ -107,7 +107,8 @@ print(json.dumps({
     "config": (f"press-only {im}x{jm}x{km}, " + ("RB omega 1.7" if a.scheme == "redblack" else "TW omega 1.0") +
                f", {a.n_iter} iterations, halo {a.halo}"),
     "sor_kernel": ({1: "k_sor_rbt", 2: "k_sor_resident", 3: "k_sor_rb"}[lib.lesb_sor_path_in_use(h.h, 0)]
-                   if a.scheme == "redblack" else "k_sor_tw"),
+                   if a.scheme == "redblack" else ("k_sor_rbt (twinned sweep)" if lib.lesb_sor_path_in_use(h.h, 0) != 3
+                                                   else "k_sor_tw")),
     "ms_per_solve": ms, "us_per_iteration": 1000 * ms / a.n_iter,
     "mcell_iter_per_s": n * a.n_iter / (ms * 1e-3) / 1e6,
     "roofline": {"bytes_per_cell_iteration": bpc, "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"],
