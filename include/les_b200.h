@@ -133,7 +133,11 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
 /* n_steps steps with one host synchronisation at the end.  inflow holds
  * n_profiles blocks of 3*km floats (u, v, w); step s uses block
  * min(s, n_profiles-1).  On a non-finite stage the first failing step
- * (0-based) and stage are reported and *steps_done counts completed steps. */
+ * (0-based) and stage are reported and *steps_done counts completed steps.
+ * The steps are enqueued before the failure is known, so after
+ * LESB_NONFINITE the fields hold the end of the last enqueued step, not the
+ * reference's state after the failing stage; callers that need that state
+ * (the reference's per-step loop) use lesb_step. */
 int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profiles,
                    int n_iter, int scheme, float omega,
                    int* steps_done, int* fail_stage);

@@ -435,7 +435,11 @@ def run_steps(state, inflow, n_steps: int, n_iter: int = 50, scheme: Scheme = Sc
     """``n_steps`` calls of ``step`` with one host synchronisation at the
     end.  ``inflow`` is one WindProfile or a sequence (one per step).  Returns
     the number of steps completed; raises NumericsError (with ``.step`` set
-    to the 0-based failing step) like the step-by-step loop would."""
+    to the 0-based failing step and the reference's stage name) like the
+    step-by-step loop would.  The steps are enqueued before a failure is
+    known: after the error the fields hold the end of the last enqueued step,
+    not the reference's state after the failing stage (use ``step`` for
+    that)."""
     g = state.grid
     profs = list(inflow) if isinstance(inflow, (list, tuple)) else [inflow]
     block = np.stack([np.concatenate(_inflow_arrays(pr, g.km)) for pr in profs]).astype(np.float32)
