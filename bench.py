@@ -356,10 +356,6 @@ def run_gpu(args):
     N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
     stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0)  # asynchronous step, bookkeeping included
-    sor_path = {1: "streaming colour passes, colour-split layout", 2: "shared-memory-resident persistent kernel",
-                3: "streaming colour passes, natural layout"}[
-        lib.lesb_sor_path_in_use(hw.h, 0)]
 
     def reinit():
         N.check(lib.lesb_copy_state(hw.h, hp.h), "copy_state")
@@ -377,6 +373,12 @@ def run_gpu(args):
         N.check(lib.lesb_step_async(hw.h, N_ITER, 0, 1.7), "step")
         since += 1
     torch.cuda.synchronize()
+    # (after the warm-up: an x-slab maps its neighbours' buffers at its first
+    # solve, which decides the solver path)
+    kps = lib.lesb_kernels_per_step(hw.h, N_ITER, 0)  # asynchronous step, bookkeeping included
+    sor_path = {1: "streaming colour passes, colour-split layout", 2: "shared-memory-resident persistent kernel",
+                3: "streaming colour passes, natural layout"}[
+        lib.lesb_sor_path_in_use(hw.h, 0)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
