@@ -97,7 +97,7 @@ inline void rbs_shape(const SplitGeo& s, int* bx, int* by) {
 // halo cells (not on a neighbour slab's plane) take the closed-form
 // halo_fn value (k: 0 -> 1, km+1 -> 0; then j periodic; then i: 0 -> 1,
 // im+1 -> 0) -- the state the reference's halo_fn leaves before pass 0.
-template <int POL>
+template <int POL, bool COPY>
 __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const float* __restrict__ p,
                                                     const float* __restrict__ rhs, float* __restrict__ ps,
                                                     float* __restrict__ rs, float* __restrict__ ps2) {
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const fl
     const long long d = c * sg.n + rb + (k >> 1);
     ps[d] = val;
     rs[d] = src_r[k];
-    if (ps2) ps2[d] = val;
+    if (COPY) ps2[d] = val;
   }
 }
 
@@ -369,7 +369,7 @@ struct RbtPlan {
   int ntj;     // tiles per plane
   int ntiles;  // tiles per pass
   int grid;    // persistent CTAs
-  int threads; // kh4 * tr / 2
+  int threads; // block size (1-D): kh4 * tr / rpt compute threads, padded to whole warps
   size_t smem; // dynamic shared memory bytes
 };
 
@@ -378,11 +378,16 @@ struct RbtPlan {
 // Rows r0 .. r0+RPT-1 of a tile staged at st (RPT even: the first row's
 // parity S0 is the tile's).  o = float offset of the thread's first cell in
 // the colour arrays (32-bit: split_supported bounds the arrays).
-template <int POL, int S0, int RPT>
+// MODE 0: red-black pass; 1: red-black pass of an x-slab with the fused
+// ghost-plane exchange; 2: twinned sweep (both colours, src -> dst).  The
+// modes are separate instantiations: the ghost and twinned code paths cost
+// registers and scheduling freedom even when not taken (31 -> 42 us per
+// pass at 512^2x90 when they were runtime branches).
+template <int POL, int S0, int RPT, int MODE>
 __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plane, int khp, int spi, float* own_g,
                                          float* oth_g, const SorC& cf, float om, const bool (&in0)[4],
                                          const bool (&in1)[4], bool lead, int i, int j, int o, int sro, int nr,
-                                         double& acc, const TileGhost& tg, bool twin) {
+                                         double& acc, const TileGhost& tg) {
   const float* s_own = st + sro;
   const float* s_rhs = s_own + plane;
   const float* s_e = s_own + 2 * plane;
@@ -395,8 +400,8 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
     const int ro = h * khp;
     const float4 C = lds4(s_own + ro), RH = lds4(s_rhs + ro);
     // x neighbours: staged, or (slab edge planes) the neighbour's words of its previous pass
-    const float4 E = tg.re ? ghost_ld4(tg.re + ro, tg.rtag, tg.sys, tg.err) : lds4(s_e + ro);
-    const float4 W = tg.rw ? ghost_ld4(tg.rw + ro, tg.rtag, tg.sys, tg.err) : lds4(s_w + ro);
+    const float4 E = (MODE == 1 && tg.re) ? ghost_ld4(tg.re + ro, tg.rtag, tg.sys, tg.err) : lds4(s_e + ro);
+    const float4 W = (MODE == 1 && tg.rw) ? ghost_ld4(tg.rw + ro, tg.rtag, tg.sys, tg.err) : lds4(s_w + ro);
     const float4 So = lds4(s_mid + ro - khp), M = lds4(s_mid + ro), N = lds4(s_mid + ro + khp);
     float val[4];
     const int go = o + ro;
@@ -406,7 +411,7 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
       rbs_row<1>(cf, om, C, RH, E, W, N, So, M, s_mid[ro + 4], in1, val, acc);
       if (POL != 0 && lead) oth_g[go] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
     }
-    if (twin && POL != 0 && lead && ((S0 + h) & 1) == 0) {
+    if (MODE == 2 && POL != 0 && lead && ((S0 + h) & 1) == 0) {
       // twinned sweep: slot 0 of this row is the k = 0 halo cell, which the
       // other colour's tile of this launch sets (its B mirror): leave it
       own_g[go + 1] = val[1];
@@ -415,8 +420,8 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
     } else {
       st4(own_g + go, val[0], val[1], val[2], val[3]);
     }
-    if (tg.pw) ghost_st4(tg.pw + ro, val, tg.wtag, tg.sys);  // straight into the neighbours' ghost planes
-    if (tg.pe) ghost_st4(tg.pe + ro, val, tg.wtag, tg.sys);
+    if (MODE == 1 && tg.pw) ghost_st4(tg.pw + ro, val, tg.wtag, tg.sys);  // straight into the neighbours' ghost planes
+    if (MODE == 1 && tg.pe) ghost_st4(tg.pe + ro, val, tg.wtag, tg.sys);
     if (wmir) st4(oth_g + go - spi, val[0], val[1], val[2], val[3]);  // W mirror: p[0,j,k] = p[1,j,k]
     if (POL == 1 || POL == 3) {  // p[i,jm+1,k] = p[i,1,k], p[i,0,k] = p[i,jm,k]
       // even jm: the same colour (own array); odd jm (twinned only, POL 3:
@@ -434,8 +439,10 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
 // POL 0: stored halo; 1: press, even jm (y mirrors into the same colour);
 // 2: press, odd jm, red-black (y halo rows refreshed before the pass);
 // 3: press, odd jm, twinned (y mirrors into the other colour of dst).
-template <int POL, int RPT>
-__global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float* src, float* dst,
+// (dst is declared __restrict__ although it equals src in the red-black
+// pass: src is read only by the TMA engine, never through a generic load)
+template <int POL, int RPT, int MODE>
+__global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float* src, float* __restrict__ dst,
                                                  const float* __restrict__ rs, SorC cf, float om, int c_fixed,
                                                  RbtPlan pl, double* __restrict__ partials, PassGhost gh) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -445,8 +452,12 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
   const int spi = (int)sg.spi;
   const int plane = pl.tr * khp;
   const int sfl = (5 * pl.tr + 2) * khp;
-  const int ncol = c_fixed < 0 ? 2 : 1;
-  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int ncol = MODE == 2 ? 2 : 1;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int ncomp = sg.kh4 * (pl.tr / RPT);  // compute threads
+  const int ncw = (ncomp + 31) >> 5;         // compute warps
+  (void)ncw;
   if (tid == 0) {
     for (int s = 0; s < pl.ns; ++s) mbar_init(&bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -456,17 +467,27 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
   // the CTA walks t = blockIdx.x + k * gridDim.x with incremental (pos, jt).
   // With the fused slab exchange the edge planes go first (position 0: plane
   // 1, position 1: plane im), so their words reach the neighbours early.
-  const bool ghosts = gh.my_w || gh.my_e;
+  const bool ghosts = MODE == 1 && (gh.my_w || gh.my_e);
   auto plane_of = [&](int pos) {
     if (!ghosts) return 1 + pos;
     return pos == 0 ? 1 : (pos == 1 ? g.im : pos);
   };
   // tile t -> (plane position, row chunk, colour)
+  // (division by ntj through a float reciprocal and one correction each way:
+  // an integer division per tile and thread cost ~7% of the pass)
+  const float rntj = 1.0f / (float)pl.ntj;
   auto decode = [&](int t, int& pos, int& jt, int& c) {
     const int r = ncol == 2 ? (t >> 1) : t;
     c = ncol == 2 ? (t & 1) : c_fixed;
-    pos = r / pl.ntj;
+    pos = __float2int_rz(((float)r + 0.5f) * rntj);
     jt = r - pos * pl.ntj;
+    if (jt < 0) {
+      --pos;
+      jt += pl.ntj;
+    } else if (jt >= pl.ntj) {
+      ++pos;
+      jt -= pl.ntj;
+    }
   };
   auto issue = [&](int t, int s) {
     int pos, jt, c;
@@ -480,7 +501,7 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
     const float* own_s = src + (long long)c * sg.n;
     const float* oth_s = src + (long long)(c ^ 1) * sg.n;
     const float* rhs_g = rs + (long long)c * sg.n;
-    const bool skip_e = gh.my_e && i == g.im, skip_w = gh.my_w && i == 1;  // from the ghost planes instead
+    const bool skip_e = MODE == 1 && gh.my_e && i == g.im, skip_w = MODE == 1 && gh.my_w && i == 1;  // ghost planes
     mbar_expect_tx(&bar[s], (skip_e ? 0u : rb) + (skip_w ? 0u : rb) + 2 * rb + rb + 2u * khp * 4);
     bulk_g2s(st, own_s + go, rb, &bar[s]);
     bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
@@ -495,10 +516,12 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
     wtag = ghost_tag(ep, gh.pass);
   }
   const int my = (pl.ntiles * ncol - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
+  double acc = 0.0;
   if (tid == 0)
     for (int k = 0; k < pl.ns && k < my; ++k) issue((int)blockIdx.x + k * (int)gridDim.x, k);
   // per-thread invariants: its slot group q, its rows r0 .. r0+RPT-1 of a tile
-  const int q = threadIdx.x, r0 = RPT * threadIdx.y;
+  const bool active = tid < ncomp;
+  const int q = active ? tid % sg.kh4 : 0, r0 = active ? RPT * (tid / sg.kh4) : pl.tr;
   bool in0[4], in1[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
@@ -508,17 +531,35 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
   }
   const bool lead = q == 0;
   const int sro = r0 * khp + 4 * q;  // the thread's offset inside a staged array
-  double acc = 0.0;
+  // the compute cursor: one colour (MODE 0, 1) walks (position, rows)
+  // incrementally by gridDim tiles; the twinned sweep decodes each tile
+  int cur_pos, cur_jt, cur_c;
+  decode((int)blockIdx.x, cur_pos, cur_jt, cur_c);
+  const int dpos = (int)gridDim.x / pl.ntj, djt = (int)gridDim.x % pl.ntj;
+  float* own_g = dst + (long long)cur_c * sg.n;
+  float* oth_g = dst + (long long)(cur_c ^ 1) * sg.n;
   for (int k = 0; k < my; ++k) {
     const int s = k % pl.ns;
     int ii, jt, c;
-    decode((int)blockIdx.x + k * (int)gridDim.x, ii, jt, c);
-    float* own_g = dst + (long long)c * sg.n;
-    float* oth_g = dst + (long long)(c ^ 1) * sg.n;
+    if (MODE == 2) {
+      decode((int)blockIdx.x + k * (int)gridDim.x, ii, jt, c);
+      own_g = dst + (long long)c * sg.n;
+      oth_g = dst + (long long)(c ^ 1) * sg.n;
+    } else {
+      ii = cur_pos;
+      jt = cur_jt;
+      c = c_fixed;
+      cur_pos += dpos;
+      cur_jt += djt;
+      if (cur_jt >= pl.ntj) {
+        cur_jt -= pl.ntj;
+        ++cur_pos;
+      }
+    }
     mbar_wait(&bar[s], (unsigned)((k / pl.ns) & 1));
     const int j = 1 + jt * pl.tr + r0;
     const int nr = g.jm - j + 1;  // rows left in the plane from the thread's first row
-    if (nr > 0) {
+    if (active && nr > 0) {
       const int pi = plane_of(ii);
       const int o = pi * spi + j * khp + 4 * q;
       const float* st = stages + s * sfl;
@@ -531,12 +572,25 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
         if (pi == 1 && gh.to_w) tg.pw = gh.to_w + ws_;
         if (pi == g.im && gh.to_e) tg.pe = gh.to_e + ws_;
       }
-      if (((c + pi + g.ioff) & 1) == 0)
-        rbt_rows<POL, 0, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
-                              tg, ncol == 2);
-      else
-        rbt_rows<POL, 1, RPT>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
-                              tg, ncol == 2);
+      // only an x-slab's edge-plane tiles take the ghost path; the others run
+      // the plain pass code (the ghost branches slow every tile otherwise)
+      constexpr int M0 = MODE == 1 ? 0 : MODE;
+      const bool gtile = MODE == 1 && (tg.rw || tg.re || tg.pw || tg.pe);
+      if (((c + pi + g.ioff) & 1) == 0) {
+        if (gtile)
+          rbt_rows<POL, 0, RPT, 1>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
+                                   tg);
+        else
+          rbt_rows<POL, 0, RPT, M0>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr,
+                                    acc, tg);
+      } else {
+        if (gtile)
+          rbt_rows<POL, 1, RPT, 1>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr, acc,
+                                   tg);
+        else
+          rbt_rows<POL, 1, RPT, M0>(g, st, plane, khp, spi, own_g, oth_g, cf, om, in0, in1, lead, pi, j, o, sro, nr,
+                                    acc, tg);
+      }
     }
     __syncthreads();  // every thread is done with stage s
     if (tid == 0 && k + pl.ns < my) {
@@ -545,10 +599,7 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
     }
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((tid & 31) == 0) {
-    const int wpb = (blockDim.x * blockDim.y + 31) >> 5;
-    partials[(long long)blockIdx.x * wpb + (tid >> 5)] = acc;
-  }
+  if (lane == 0) partials[(long long)blockIdx.x * ((blockDim.x + 31) >> 5) + (tid >> 5)] = acc;
 }
 
 // Pre-pass snapshot of the y halo rows (press policy, odd jm): the colour-c
@@ -609,8 +660,13 @@ void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* sp
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
   const unsigned nb = (unsigned)((nrow + 7) / 8);
-  if (policy == 1) k_split_pack<1><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
-  else k_split_pack<0><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+  if (p_copy) {
+    if (policy == 1) k_split_pack<1, true><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+    else k_split_pack<0, true><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+  } else {
+    if (policy == 1) k_split_pack<1, false><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, nullptr);
+    else k_split_pack<0, false><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, nullptr);
+  }
 }
 
 static dim3 rbs_grid(const Geo& g, const SplitGeo& sg, int* bx, int* by) {
@@ -638,7 +694,8 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
   static const int env_tr = std::getenv("LESB_RBT_TR") ? std::atoi(std::getenv("LESB_RBT_TR")) : 0;
   static const int env_ns = std::getenv("LESB_RBT_NS") ? std::atoi(std::getenv("LESB_RBT_NS")) : 0;
   static const int env_rpt = std::getenv("LESB_RBT_RPT") ? std::atoi(std::getenv("LESB_RBT_RPT")) : 0;
-  const int rpt = env_rpt == 4 ? 4 : 2;
+  const int rpt = 2;  // (4 rows per thread measured slower; RBT_RPT kept as a template parameter)
+  (void)env_rpt;
   int tr = env_tr > 0 ? env_tr : rpt * (512 / (2 * sg.kh4));
   tr = std::max(rpt, tr - tr % rpt);
   while (tr > rpt && sg.kh4 * (tr / rpt) > 512) tr -= rpt;
@@ -647,8 +704,9 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
   while (ns > 2 && 128 + ns * stage > 200 * 1024) --ns;
   pl.rpt = rpt;
   pl.tr = tr;
-  pl.ns = ns;
-  pl.threads = sg.kh4 * (tr / rpt);
+  pl.ns = std::min(ns, 8);
+  // whole warps (the residual is shuffle-reduced per warp): padding threads compute nothing
+  pl.threads = ((sg.kh4 * (tr / rpt) + 31) / 32) * 32;
   pl.smem = 128 + ns * stage;
   pl.ntj = (g.jm + tr - 1) / tr;
   pl.ntiles = pl.ntj * g.im;
@@ -657,17 +715,14 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sor_rbt<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sor_rbt<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#define RBT_ATTR(P, M) cudaFuncSetAttribute(k_sor_rbt<P, 2, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+    RBT_ATTR(0, 0); RBT_ATTR(1, 0); RBT_ATTR(2, 0);
+    RBT_ATTR(0, 1); RBT_ATTR(1, 1); RBT_ATTR(2, 1);
+    RBT_ATTR(0, 2); RBT_ATTR(1, 2); RBT_ATTR(3, 2);
+#undef RBT_ATTR
     attr = true;
   }
-  if (rpt == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 4>, pl.threads, pl.smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 2>, pl.threads, pl.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 2, 1>, pl.threads, pl.smem);
   if (per < 1) per = 1;
   pl.grid = std::min(pl.ntiles, sms * per);
   return pl;
@@ -729,16 +784,19 @@ void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c
     k_split_refresh_y<<<dim3((sg.khp + 127) / 128, g.im), 128, 0, st>>>(g, sg, split, c);
   if (rbt_ok(sg)) {
     const RbtPlan pl = rbt_plan(g, sg);
-    const dim3 block(sg.kh4, pl.tr / pl.rpt);
-    if (pl.rpt == 4) {
-      if (pol == 2) k_sor_rbt<2, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
-      else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
-      else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+    const dim3 block(pl.threads);
+    const bool gho = gh.my_w || gh.my_e;
+#define RBT_GO(P, M) k_sor_rbt<P, 2, M><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh)
+    if (gho) {
+      if (pol == 2) RBT_GO(2, 1);
+      else if (pol == 1) RBT_GO(1, 1);
+      else RBT_GO(0, 1);
     } else {
-      if (pol == 2) k_sor_rbt<2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
-      else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
-      else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh);
+      if (pol == 2) RBT_GO(2, 0);
+      else if (pol == 1) RBT_GO(1, 0);
+      else RBT_GO(0, 0);
     }
+#undef RBT_GO
     return;
   }
   int bx, by;
@@ -766,18 +824,14 @@ void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* r
                       int policy, double* partials, cudaStream_t st) {
   const SplitGeo sg = split_geo(g);
   const RbtPlan pl = rbt_plan(g, sg);
-  const dim3 block(sg.kh4, pl.tr / pl.rpt);
+  const dim3 block(pl.threads);
   const PassGhost gh{};
   const int pol = policy == 1 ? ((g.jm & 1) ? 3 : 1) : 0;
-  if (pl.rpt == 4) {
-    if (pol == 3) k_sor_rbt<3, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-    else if (pol == 1) k_sor_rbt<1, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-    else k_sor_rbt<0, 4><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-  } else {
-    if (pol == 3) k_sor_rbt<3, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-    else if (pol == 1) k_sor_rbt<1, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-    else k_sor_rbt<0, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh);
-  }
+#define RBT_TW(P) k_sor_rbt<P, 2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh)
+  if (pol == 3) RBT_TW(3);
+  else if (pol == 1) RBT_TW(1);
+  else RBT_TW(0);
+#undef RBT_TW
 }
 
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st) {
