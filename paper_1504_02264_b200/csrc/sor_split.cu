@@ -411,9 +411,10 @@ __device__ __forceinline__ void rbt_rows(const Geo& g, const float* st, int plan
       rbs_row<1>(cf, om, C, RH, E, W, N, So, M, s_mid[ro + 4], in1, val, acc);
       if (POL != 0 && lead) oth_g[go] = val[0];  // B mirror: p[i,j,0] = p[i,j,1]
     }
-    if (MODE == 2 && POL != 0 && lead && ((S0 + h) & 1) == 0) {
-      // twinned sweep: slot 0 of this row is the k = 0 halo cell, which the
-      // other colour's tile of this launch sets (its B mirror): leave it
+    if (POL != 0 && lead && ((S0 + h) & 1) == 0) {
+      // slot 0 of this row is the k = 0 halo cell, set by the other colour's
+      // B mirror (twinned: in this launch; red-black: in the previous pass,
+      // possibly after this tile's early load): leave it
       own_g[go + 1] = val[1];
       own_g[go + 2] = val[2];
       own_g[go + 3] = val[3];
@@ -489,7 +490,12 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
       jt -= pl.ntj;
     }
   };
-  auto issue = [&](int t, int s) {
+  // part: 1 = own cells + rhs (+ the stage's whole expect_tx), 2 = the other
+  // colour's rows, 3 = both.  In a red-black pass (MODE 0) part 1 depends
+  // on no earlier launch (the own colour was last written two passes ago;
+  // the slot the previous pass's B mirror writes is never stored back from a
+  // load), so it is issued before griddepcontrol.wait.
+  auto issue = [&](int t, int s, int part = 3) {
     int pos, jt, c;
     decode(t, pos, jt, c);
     const int i = plane_of(pos);
@@ -502,13 +508,28 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
     const float* oth_s = src + (long long)(c ^ 1) * sg.n;
     const float* rhs_g = rs + (long long)c * sg.n;
     const bool skip_e = MODE == 1 && gh.my_e && i == g.im, skip_w = MODE == 1 && gh.my_w && i == 1;  // ghost planes
-    mbar_expect_tx(&bar[s], (skip_e ? 0u : rb) + (skip_w ? 0u : rb) + 2 * rb + rb + 2u * khp * 4);
-    bulk_g2s(st, own_s + go, rb, &bar[s]);
-    bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
-    if (!skip_e) bulk_g2s(st + 2 * plane, oth_s + go + spi, rb, &bar[s]);
-    if (!skip_w) bulk_g2s(st + 3 * plane, oth_s + go - spi, rb, &bar[s]);
-    bulk_g2s(st + 4 * plane, oth_s + go - khp, rb + 2u * khp * 4, &bar[s]);
+    if (part & 1) {
+      mbar_expect_tx(&bar[s], (skip_e ? 0u : rb) + (skip_w ? 0u : rb) + 2 * rb + rb + 2u * khp * 4);
+      bulk_g2s(st, own_s + go, rb, &bar[s]);
+      bulk_g2s(st + plane, rhs_g + go, rb, &bar[s]);
+    }
+    if (part & 2) {
+      if (!skip_e) bulk_g2s(st + 2 * plane, oth_s + go + spi, rb, &bar[s]);
+      if (!skip_w) bulk_g2s(st + 3 * plane, oth_s + go - spi, rb, &bar[s]);
+      bulk_g2s(st + 4 * plane, oth_s + go - khp, rb + 2u * khp * 4, &bar[s]);
+    }
   };
+  // programmatic dependent launch: this grid may have started while the
+  // previous launch drains; the own cells and rhs of the first tiles depend
+  // on no launch later than the one before the previous (whose completion
+  // the previous launch waited for before it let this grid start)
+  const int my0 = (pl.ntiles * ncol - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (MODE == 0 && tid == 0)
+    for (int k = 0; k < pl.ns && k < my0; ++k) issue((int)blockIdx.x + k * (int)gridDim.x, k, 1);
+  // everything below may read what the previous launch wrote; only then may
+  // the next launch start (so its early loads see this grid's predecessor)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   unsigned rtag = 0, wtag = 0;
   if (ghosts) {
     const unsigned ep = *(volatile const unsigned*)gh.epoch;
@@ -518,7 +539,7 @@ __global__ void __launch_bounds__(512) k_sor_rbt(Geo g, SplitGeo sg, const float
   const int my = (pl.ntiles * ncol - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
   double acc = 0.0;
   if (tid == 0)
-    for (int k = 0; k < pl.ns && k < my; ++k) issue((int)blockIdx.x + k * (int)gridDim.x, k);
+    for (int k = 0; k < pl.ns && k < my; ++k) issue((int)blockIdx.x + k * (int)gridDim.x, k, MODE == 0 ? 2 : 3);
   // per-thread invariants: its slot group q, its rows r0 .. r0+RPT-1 of a tile
   const bool active = tid < ncomp;
   const int q = active ? tid % sg.kh4 : 0, r0 = active ? RPT * (tid / sg.kh4) : pl.tr;
@@ -786,8 +807,27 @@ void launch_rbs_pass(const Geo& g, float* split, const SorC& cf, float om, int c
     const RbtPlan pl = rbt_plan(g, sg);
     const dim3 block(pl.threads);
     const bool gho = gh.my_w || gh.my_e;
-#define RBT_GO(P, M) k_sor_rbt<P, 2, M><<<pl.grid, block, pl.smem, st>>>(g, sg, ps, ps, rs, cf, om, c, pl, partials, gh)
+    // programmatic stream serialisation: the pass may start while the
+    // previous launch drains (its griddepcontrol.wait orders the dependent
+    // accesses); LESB_PDL=0 launches it plainly
+    static const bool pdl = !(std::getenv("LESB_PDL") && std::atoi(std::getenv("LESB_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const float* cps = ps;
+#define RBT_GO(P, M) cudaLaunchKernelEx(&cfg, k_sor_rbt<P, 2, M>, g, sg, cps, ps, (const float*)rs, cf, om, c, pl, partials, gh)
     if (gho) {
+      // (no early start for the slab passes: in one process the slabs' grids
+      // share the SMs, and early CTAs parked at griddepcontrol.wait hold slots
+      // another slab's pass needs -- 2 slabs of 600x300x90: +24% vs +8%)
+      cfg.numAttrs = 0;
       if (pol == 2) RBT_GO(2, 1);
       else if (pol == 1) RBT_GO(1, 1);
       else RBT_GO(0, 1);
@@ -827,7 +867,18 @@ void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* r
   const dim3 block(pl.threads);
   const PassGhost gh{};
   const int pol = policy == 1 ? ((g.jm & 1) ? 3 : 1) : 0;
-#define RBT_TW(P) k_sor_rbt<P, 2, 2><<<pl.grid, block, pl.smem, st>>>(g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh)
+  static const bool pdl = !(std::getenv("LESB_PDL") && std::atoi(std::getenv("LESB_PDL")) == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;  // (a sweep waits for the previous one before any access)
+#define RBT_TW(P) cudaLaunchKernelEx(&cfg, k_sor_rbt<P, 2, 2>, g, sg, src, dst, rhs_split, cf, om, -1, pl, partials, gh)
   if (pol == 3) RBT_TW(3);
   else if (pol == 1) RBT_TW(1);
   else RBT_TW(0);
