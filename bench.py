@@ -353,7 +353,10 @@ def run_gpu(args):
         hw, hp = _H(slab_dom.slab.h), _H(pristine.h)
     arrs = [N.f32c(getattr(inflow, c)) for c in ("u", "v", "w")]
     N.check(lib.lesb_set_inflow(hw.h, *[N.fptr(a) for a in arrs]), "set_inflow")
-    N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
+    # the timed steps replay the plain step graph; the phase split comes from
+    # a separate, shorter run of the graph variant with event records between
+    # the phases (instrumentation, not part of the measured steps)
+    N.check(lib.lesb_set_timing(hw.h, 0), "set_timing")
     stream = torch.cuda.ExternalStream(lib.lesb_stream(hw.h))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -395,11 +398,25 @@ def run_gpu(args):
             with torch.cuda.stream(stream):
                 ev[s][1].record(stream)
             since += 1
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    # phase split: the instrumented graph, L2 flushed before each step as above
+    N.check(lib.lesb_set_timing(hw.h, 1), "set_timing")
+    n_ph = min(args.steps, 10)
+    for s in range(n_ph + 1):
+        if since == REINIT:
+            reinit()
+            since = 0
+        with torch.cuda.stream(stream):
+            flush.fill_(float(s))
+        N.check(lib.lesb_step_async(hw.h, N_ITER, 0, 1.7), "step")
+        since += 1
+        if s > 0:  # (the first replay builds the instrumented graph)
             ph = np.zeros(4, np.float32)
             N.check(lib.lesb_last_step_times(hw.h, N.fptr(ph)), "times")
             phase_ms += ph
-        torch.cuda.synchronize()
-    wall = time.perf_counter() - t_wall
+    torch.cuda.synchronize()
+    N.check(lib.lesb_set_timing(hw.h, 0), "set_timing")
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -419,7 +436,7 @@ def run_gpu(args):
     value = world * args.steps / (dev_ms / 1000.0)  # slab-steps over all ranks / max time
     n_int = IM * JM * KM
     hbm, peak_kind = peaks()
-    phase_ms /= args.steps
+    phase_ms /= n_ph
     # dominant kernel: the SOR solve (phase 2 = the solver launches between the
     # step's fused kernel and the press halo).  Algorithmic bytes: 12 B per
     # interior cell and iteration (SURVEY 8(d), cn1 scalar) x N x n_iter.

@@ -63,13 +63,19 @@ namespace cg = cooperative_groups;
 
 namespace lesb {
 
-constexpr int RES_THREADS = 512;
+#ifndef RES_NTHREADS
+#define RES_NTHREADS 512
+#endif
+constexpr int RES_THREADS = RES_NTHREADS;
 constexpr int RES_WARPS = RES_THREADS / 32;
 constexpr int NST = 6;   // LESB_RES_TRACE stamps per pass
 #ifndef RES_RU
 #define RES_RU 4
 #endif
-constexpr int RCVP = 3;  // receive slot pairs each thread keeps in registers  // face values each thread has in flight while receiving
+#ifndef RES_RCVP
+#define RES_RCVP 3
+#endif
+constexpr int RCVP = RES_RCVP;  // receive slot pairs each thread keeps in registers
 
 struct ResPlan {
   int ni, nj;       // tile grid
@@ -277,6 +283,81 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
   return acc;
 }
 
+// One run of slot PAIRS j0 <= j < j1 of one column (slots 2j, 2j + 1 of the
+// colour-nrd array): six 64-bit shared loads (centre, E, W, N, S, rhs) and
+// three words of the other colour's top/bottom chain per pair.  Every lane
+// of a warp is at the same slot offset of its column, so the 64-bit accesses
+// are parity independent and conflict free for the plan's row pad
+// (interior_bank_load), unlike the per-cell walk (update_run) whose centre
+// slot alternates with the column parity (measured there: 2.1x the ideal
+// shared-memory wavefronts, the kernel's bound at 150^2x90; pair runs
+// 383 -> 345 us per 50-iteration solve).
+#ifndef RES_IPAIRS
+#define RES_IPAIRS 1
+#endif
+
+template <bool PRESS>
+__device__ __forceinline__ double update_prun(const ResArgs& a, float* S, unsigned ci, int j0, int j1, int nrd,
+                                              int KK, int CW, int sI, int km) {
+  const int cb = (int)(ci & CB_MASK);
+  const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
+  const bool wphys = PRESS && (ci & (1u << 29));
+  // slot s holds k = 2 s + kp: pair j has a cell while 4 j + kp <= km
+  const int jmax = (km - kp) >> 2;
+  if (j1 > jmax + 1) j1 = jmax + 1;
+  double acc = 0.0;
+  if (j0 >= j1) return acc;
+  float* const ce0 = S + cb + nrd * KK;        // colour-nrd array of the column
+  const float* const ob = S + cb + (1 - nrd) * KK;  // the other colour's
+  // the other colour's slot s holds k = 2 s + 1 - kp: for the pair at slot
+  // s0 the chain bottom, k+-1 between the cells, top is ob[s0 + kp - 1 + 0..2]
+  auto pair = [&](int s0, float pB0, float pTB, float pT1, bool v0, bool v1, bool bottom) -> double {
+    float* ce = ce0 + s0;
+    const float* o = ob + s0;
+    const float2 c2 = *reinterpret_cast<const float2*>(ce);
+    const float2 e2 = *reinterpret_cast<const float2*>(o + sI);
+    const float2 w2 = *reinterpret_cast<const float2*>(o - sI);
+    const float2 n2 = *reinterpret_cast<const float2*>(o + CW);
+    const float2 s2 = *reinterpret_cast<const float2*>(o - CW);
+    const float2 r2 = *reinterpret_cast<const float2*>(ce + 2 * KK);
+    float pW0 = w2.x, pW1 = w2.y;
+    if (PRESS) {
+      if (wphys) {  // physical west: p[0] -> p[1]
+        pW0 = c2.x;
+        pW1 = c2.y;
+      }
+      if (bottom) pB0 = c2.x;  // bottom: p[.,.,0] -> p[.,.,1]
+    }
+    // sor.py:164-171: E, W, N, S, T, B summed left to right
+    float nb0 = a.w2l * e2.x, nb1 = a.w2l * e2.y;
+    nb0 = nb0 + a.w2s * pW0;
+    nb1 = nb1 + a.w2s * pW1;
+    nb0 = nb0 + a.w3l * n2.x;
+    nb1 = nb1 + a.w3l * n2.y;
+    nb0 = nb0 + a.w3s * s2.x;
+    nb1 = nb1 + a.w3s * s2.y;
+    nb0 = nb0 + a.w4l * pTB;
+    nb1 = nb1 + a.w4l * pT1;
+    nb0 = nb0 + a.w4s * pB0;
+    nb1 = nb1 + a.w4s * pTB;
+    // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+    const float rel0 = a.om * (a.cn1 * (nb0 - r2.x) - c2.x);
+    const float rel1 = a.om * (a.cn1 * (nb1 - r2.y) - c2.y);
+    *reinterpret_cast<float2*>(ce) = make_float2(v0 ? c2.x + rel0 : c2.x, v1 ? c2.y + rel1 : c2.y);
+    return (v0 ? (double)rel0 * (double)rel0 : 0.0) + (v1 ? (double)rel1 * (double)rel1 : 0.0);
+  };
+  // (measured: a separate unchecked loop for the pairs between the column
+  // ends, with the chain carried in registers, was 2% slower)
+  auto edge = [&](int j) {
+    const int s0 = 2 * j;
+    const int lo = s0 + kp - 1;  // (clamped into the array: a clamped word is never used)
+    const float pB0 = ob[max(lo, 0)], pTB = ob[lo + 1], pT1 = ob[min(lo + 2, KK - 1)];
+    return pair(s0, pB0, pTB, pT1, s0 + kp >= 1, 2 * s0 + 2 + kp <= km, s0 == 0 && kp == 1);
+  };
+  for (int j = j0; j < j1; ++j) acc += edge(j);
+  return acc;
+}
+
 // Boundary phase over slot PAIRS: unit w = (c - c0) * HP + j goes to thread
 // w % nth and updates the colour-nrd cells in slots 2j, 2j + 1 of column c
 // (one column decode per two cells, the bottom neighbour of the second cell
@@ -397,12 +478,13 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
 }
 
 // All runs of this thread in columns [c0, c1): the columns are cut into nseg
-// runs of L cells and run u = g * (c1 - c0) + (c - c0) goes to thread
-// u % nth.  Column-fastest numbering puts a warp's lanes in consecutive
-// columns at the same slot offset; with the odd column stride their shared
-// addresses fall in distinct banks.
-// (g, cc): the segment and column of this thread's first run; (dg, dcc):
-// RES_THREADS runs on -- decoded once before the pass loop.
+// runs of L work items (the last run of a column the shortest) and run
+// u = g * (c1 - c0) + (c - c0) goes to thread (u - rot) mod U, U = nseg (c1 - c0):
+// rot = (nseg - 1)(c1 - c0) hands the short last runs to the lowest threads,
+// which are the ones with an extra boundary pair.  Column-fastest numbering
+// puts a warp's lanes in consecutive columns at the same slot offset.
+// (g, cc): the segment and column of this thread's first run, nu its run
+// count; (dg, dcc): RES_THREADS runs on -- decoded once before the pass loop.
 // mid() runs once, part-way through the thread's first run (or first, when
 // the thread has none): it issues the next pass's receive loads, so their
 // L2 round trip overlaps the rest of the interior.
@@ -411,15 +493,27 @@ __device__ __forceinline__ double update_boundary(const ResArgs& a, float* S, co
 #endif
 template <bool PRESS, class F>
 __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const unsigned* __restrict__ coltab,
-                                               int c0, int c1, int nseg, int g, int cc, int dg, int dcc, int L,
-                                               int KT, int nrd, int KK, int CW, int sI, int km, F&& mid) {
+                                               int c0, int c1, int nseg, int g, int cc, int nu, int dg, int dcc,
+                                               int L, int KT, int nrd, int KK, int CW, int sI, int km, F&& mid) {
   double acc = 0.0;
   const int ncc = c1 - c0;
   bool issued = false;
-  while (g < nseg) {
+  for (; nu > 0; --nu) {
     const int t0 = g * L;
     const int t1 = min(t0 + L, KT);
     const unsigned ci = coltab[c0 + cc];
+#if RES_IPAIRS
+    // (t0, t1): slot pairs
+    if (!issued) {
+      const int tm = t0 + ((t1 - t0) >> 1);
+      acc += update_prun<PRESS>(a, S, ci, t0, tm, nrd, KK, CW, sI, km);
+      mid();
+      issued = true;
+      acc += update_prun<PRESS>(a, S, ci, tm, t1, nrd, KK, CW, sI, km);
+    } else {
+      acc += update_prun<PRESS>(a, S, ci, t0, t1, nrd, KK, CW, sI, km);
+    }
+#else
     if (!issued) {
       constexpr int RU = RES_RU;
       const int h = (t1 - t0) >> 1;
@@ -431,12 +525,14 @@ __device__ __forceinline__ double update_phase(const ResArgs& a, float* S, const
     } else {
       acc += update_run<PRESS>(a, S, ci, t0, t1, nrd, KK, CW, sI, km);
     }
+#endif
     g += dg;
     cc += dcc;
     if (cc >= ncc) {
       cc -= ncc;
       ++g;
     }
+    if (g >= nseg) g -= nseg;
   }
   if (!issued) mid();
   return acc;
@@ -558,6 +654,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
                           (si_ + g.ioff + sj_) & 1);
   }
 
+  // (programmatic dependent launch: everything above used only the launch
+  // parameters; p and rhs are the previous kernel's output)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
   // ---- load tile columns, rhs and halo columns from global memory (warp per
   // column).  Every element is an asynchronous 4-byte copy (cp.async, zero-fill
   // where the value is a constant 0), so all of a thread's loads are in flight
@@ -610,11 +710,16 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   if (tx && tid == 0) tx[7] = gtimer();
   // runs: every thread gets about one boundary run and one interior run
   const int nint = ncol - nbnd;
-  const int nseg_i = max(1, min(KT, nint > 0 ? nth / nint : 1));
-  const int L_i = (KT + nseg_i - 1) / nseg_i;
+  // interior work items per column: cells (update_run) or slot pairs (update_prun)
+  const int KTI = RES_IPAIRS ? (KK >> 1) : KT;
+  const int nseg_i = max(1, min(KTI, nint > 0 ? nth / nint : 1));
+  const int L_i = (KTI + nseg_i - 1) / nseg_i;
   // pass-invariant decode of this thread's first interior run / boundary pair
   const int nint1 = max(nint, 1);
-  const int ig0 = nint > 0 ? tid / nint1 : nseg_i, icc0 = tid - (tid / nint1) * nint1;
+  const int U_i = nseg_i * nint;  // interior runs
+  const int iu0 = tid + (nseg_i - 1) * nint >= U_i ? tid + (nseg_i - 1) * nint - U_i : tid + (nseg_i - 1) * nint;
+  const int inu = tid < U_i ? (U_i - 1 - tid) / nth + 1 : 0;
+  const int ig0 = iu0 / nint1, icc0 = iu0 - ig0 * nint1;
   const int idg = nth / nint1, idcc = nth - idg * nint1;
   const int HPb = KKF >> 1;
   const int bc0 = tid / HPb, bj0 = tid - bc0 * HPb, bdq = nth / HPb, bdr = nth - bdq * HPb;
@@ -759,7 +864,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
                                          KK, CW, sI, km);
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!RES_DBG(a, 2))
-      acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, idg, idcc, L_i, KT, nrd, KK, CW, sI, km,
+      acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, inu, idg, idcc, L_i, KTI, nrd, KK, CW, sI,
+                                 km,
                                  [&] {
                                    if (n + 1 < 2 * a.n_iter) issue_receive(n + 1);
                                  });
@@ -873,11 +979,25 @@ static int interior_bank_load(int TI, int TJ, int kk, int pad) {
     for (int w0 = 0; w0 < nint; w0 += 32) {
       int cnt[32] = {0};
       int mx = 0;
-      for (int r = w0; r < nint && r < w0 + 32; ++r) {
-        const int li = 2 + r / nj, lj = 2 + r % nj;
-        const int kp = (nrd + ((li + lj) & 1) + 1) & 1;
-        const int b = (li * sI + lj * cw + nrd * kk + (1 - kp)) & 31;
-        mx = ++cnt[b] > mx ? cnt[b] : mx;
+      if (RES_IPAIRS) {
+        // pair runs: 64-bit accesses at the same slot of every lane's column,
+        // one wavefront per half-warp when the 8-byte words hit distinct banks
+        for (int h0 = w0; h0 < nint && h0 < w0 + 32; h0 += 16) {
+          int c16[16] = {0}, m16 = 0;
+          for (int r = h0; r < nint && r < h0 + 16; ++r) {
+            const int li = 2 + r / nj, lj = 2 + r % nj;
+            const int b = ((li * sI + lj * cw + nrd * kk) >> 1) & 15;
+            m16 = ++c16[b] > m16 ? c16[b] : m16;
+          }
+          mx += m16;
+        }
+      } else {
+        for (int r = w0; r < nint && r < w0 + 32; ++r) {
+          const int li = 2 + r / nj, lj = 2 + r % nj;
+          const int kp = (nrd + ((li + lj) & 1) + 1) & 1;
+          const int b = (li * sI + lj * cw + nrd * kk + (1 - kp)) & 31;
+          mx = ++cnt[b] > mx ? cnt[b] : mx;
+        }
       }
       load += mx;
     }
@@ -999,7 +1119,24 @@ static cudaError_t launch_group(ResGroup& grp, int policy, bool slab, size_t sme
   void* args[] = {&grp};
   const void* fn = policy == 1 ? (slab ? (const void*)k_sor_resident<true, true> : (const void*)k_sor_resident<true, false>)
                                : (slab ? (const void*)k_sor_resident<false, true> : (const void*)k_sor_resident<false, false>);
-  return cudaLaunchCooperativeKernel(fn, dim3(grp.n * grp.tps), dim3(RES_THREADS), args, smem, st);
+  // programmatic dependent launch: the CTAs may start (and build their
+  // tables) while the step's fused kernel drains; griddepcontrol.wait in the
+  // kernel orders every global access after it.  LESB_STEP_PDL=0: plain.
+  static const bool pdl = !(std::getenv("LESB_STEP_PDL") && std::atoi(std::getenv("LESB_STEP_PDL")) == 0);
+  if (!pdl) return cudaLaunchCooperativeKernel(fn, dim3(grp.n * grp.tps), dim3(RES_THREADS), args, smem, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grp.n * grp.tps);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 static ResArgs make_args(const ResidentCall& c, const ResPlan& pl) {

@@ -10,6 +10,8 @@
 //    it covers, and raises that stage's non-finite bit when the value is not
 //    finite (les.py:384-390 semantics, checked inductively: all six fields are
 //    finite when a step starts).
+#include <cstdlib>
+
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
 
@@ -117,6 +119,9 @@ __global__ void k_velnw_bondv1(Geo g, Spac s, const float* __restrict__ u, const
                                const float* __restrict__ fgh, float dt, const float* __restrict__ inflow,
                                float* __restrict__ ub, float* __restrict__ vb, float* __restrict__ wb,
                                unsigned* flags) {
+  // the fused kernel that follows may be scheduled now (it waits for this
+  // grid's completion before its first access: programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int j = blockIdx.y * blockDim.y + threadIdx.y;
   int i = blockIdx.z;
@@ -396,6 +401,10 @@ __global__ void __launch_bounds__(128) k_fused_rhs(Geo g, Spac s, const float* _
                             float* __restrict__ va, float* __restrict__ wa, float* __restrict__ rhs, float vn,
                             float dt, int do_les, const float* __restrict__ csd2f, float csd2s,
                             unsigned* flags) {
+  // programmatic dependent launch (launch_fused_rhs): every input is the
+  // previous kernel's output or follows it in stream order
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   int j = blockIdx.y * blockDim.y + threadIdx.y;
   int i = blockIdx.z;
@@ -565,12 +574,23 @@ void launch_fused_rhs(const Geo& g, const Spac& s, const float* ub, const float*
   // small blocks retire without waiting on a slow sibling warp)
   const dim3 bl(32, 4, 1);
   const dim3 gr((g.km + 2 + 31) / 32, (g.jm + 2 + 3) / 4, g.im + 2);
+  // programmatic dependent launch after velnw + bondv1 (LESB_STEP_PDL=0: plain)
+  static const bool pdl = !(std::getenv("LESB_STEP_PDL") && std::atoi(std::getenv("LESB_STEP_PDL")) == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = gr;
+  cfg.blockDim = bl;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (s.p2)
-    k_fused_rhs<true><<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
-                                         csd2f, csd2s, flags);
+    cudaLaunchKernelEx(&cfg, k_fused_rhs<true>, g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
+                       csd2f, csd2s, flags);
   else
-    k_fused_rhs<false><<<gr, bl, 0, st>>>(g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt, do_les,
-                                          csd2f, csd2s, flags);
+    cudaLaunchKernelEx(&cfg, k_fused_rhs<false>, g, s, ub, vb, wb, mask, fgh, fgh_old, ua, va, wa, rhs, vn, dt,
+                       do_les, csd2f, csd2s, flags);
 }
 
 void launch_check_finite(const float* a, long long n, unsigned* flags, unsigned bit, cudaStream_t st) {
