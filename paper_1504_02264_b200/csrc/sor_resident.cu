@@ -293,7 +293,7 @@ __device__ __forceinline__ double update_run(const ResArgs& a, float* S, unsigne
 // shared-memory wavefronts, the kernel's bound at 150^2x90; pair runs
 // 383 -> 345 us per 50-iteration solve).
 #ifndef RES_IPAIRS
-#define RES_IPAIRS 1
+#define RES_IPAIRS RES_PAIRS  // (64-bit accesses need the pair layout)
 #endif
 
 template <bool PRESS>
@@ -307,7 +307,7 @@ __device__ __forceinline__ double update_prun(const ResArgs& a, float* S, unsign
   if (j1 > jmax + 1) j1 = jmax + 1;
   double acc = 0.0;
   if (j0 >= j1) return acc;
-  float* const ce0 = S + cb + nrd * KK;        // colour-nrd array of the column
+  float* const ce0 = S + cb + nrd * KK;             // colour-nrd array of the column
   const float* const ob = S + cb + (1 - nrd) * KK;  // the other colour's
   // the other colour's slot s holds k = 2 s + 1 - kp: for the pair at slot
   // s0 the chain bottom, k+-1 between the cells, top is ob[s0 + kp - 1 + 0..2]
@@ -346,15 +346,119 @@ __device__ __forceinline__ double update_prun(const ResArgs& a, float* S, unsign
     *reinterpret_cast<float2*>(ce) = make_float2(v0 ? c2.x + rel0 : c2.x, v1 ? c2.y + rel1 : c2.y);
     return (v0 ? (double)rel0 * (double)rel0 : 0.0) + (v1 ? (double)rel1 * (double)rel1 : 0.0);
   };
-  // (measured: a separate unchecked loop for the pairs between the column
-  // ends, with the chain carried in registers, was 2% slower)
-  auto edge = [&](int j) {
+  // every pair in the checked form (measured: a separate unchecked loop for
+  // the pairs between the column ends, with the chain carried in registers,
+  // was 2% slower, and one with pointer increments 4%)
+  for (int j = j0; j < j1; ++j) {
     const int s0 = 2 * j;
     const int lo = s0 + kp - 1;  // (clamped into the array: a clamped word is never used)
     const float pB0 = ob[max(lo, 0)], pTB = ob[lo + 1], pT1 = ob[min(lo + 2, KK - 1)];
-    return pair(s0, pB0, pTB, pT1, s0 + kp >= 1, 2 * s0 + 2 + kp <= km, s0 == 0 && kp == 1);
-  };
-  for (int j = j0; j < j1; ++j) acc += edge(j);
+    acc += pair(s0, pB0, pTB, pT1, s0 + kp >= 1, 2 * s0 + 2 + kp <= km, s0 == 0 && kp == 1);
+  }
+  return acc;
+}
+
+// Boundary phase from a per-unit table (RES_BTAB): unit w = c HP + j goes to
+// thread w % nth as in update_boundary, but everything about the unit that
+// does not change between passes -- column base + slot, column parity and
+// west-physical bits, the pair's cell validity and chain clamps for either
+// colour, the two face word offsets -- sits in one 16-byte entry, written by
+// the thread that uses it before the pass loop.  (The per-pass decode of
+// update_boundary cost as many instructions as the arithmetic.)
+#ifndef RES_BTAB
+#define RES_BTAB RES_PAIRS
+#endif
+// entry.w bits, per kp = 0 / 1 (shift 4 kp): v0, v1, far end of the chain clamped
+constexpr int BT_V0 = 1, BT_V1 = 2, BT_CL = 4, BT_BOT = 1 << 8;  // BT_BOT: slot 0 (press bottom when kp = 1)
+
+__device__ __forceinline__ int4 btab_entry(unsigned ci, int2 pub, int j, int KK, int km) {
+  const int s0 = 2 * j;
+  int bits = (s0 == 0) ? BT_BOT : 0;
+#pragma unroll
+  for (int kp = 0; kp < 2; ++kp) {
+    int b = 0;
+    if (s0 + kp >= 1 && 2 * s0 + kp <= km) b |= BT_V0;
+    if (2 * s0 + 2 + kp <= km) b |= BT_V1;
+    if (kp ? s0 + 2 >= KK : s0 == 0) b |= BT_CL;
+    bits |= b << (4 * kp);
+  }
+  return make_int4((int)(ci + (unsigned)s0), pub.x >= 0 ? pub.x + s0 : -1, pub.y >= 0 ? pub.y + s0 : -1, bits);
+}
+
+template <bool PRESS, bool SLAB>
+__device__ __forceinline__ double update_boundary_tab(const ResArgs& a, float* S, const int4* __restrict__ btab,
+                                                   int nbu, unsigned long long* X, unsigned long long* XRw,
+                                                   unsigned long long* XRe, unsigned tag, int nrd, int KK, int CW,
+                                                   int sI) {
+  double acc = 0.0;
+  float* const Sc = S + nrd * KK;
+  const float* const So = S + (1 - nrd) * KK;
+  const unsigned long long tagw = (unsigned long long)tag << 32;
+  for (int w = threadIdx.x; w < nbu; w += RES_THREADS) {
+    const int4 d = btab[w];
+    const unsigned ci = (unsigned)d.x;
+    const int kp = (nrd + (int)((ci >> 28) & 1u) + 1) & 1;
+    const int vb = d.w >> (4 * kp);
+    const bool v0 = vb & BT_V0, v1 = vb & BT_V1;
+    if (!(v0 || v1)) continue;
+    const int off = (int)(ci & CB_MASK);  // column base + s0
+    float* ce = Sc + off;
+    const float* o = So + off;            // other colour, same k as slot s0
+    const float2 c2 = *reinterpret_cast<const float2*>(ce);
+    const float2 e2 = *reinterpret_cast<const float2*>(o + sI);
+    const float2 w2 = *reinterpret_cast<const float2*>(o - sI);
+    const float2 n2 = *reinterpret_cast<const float2*>(o + CW);
+    const float2 s2 = *reinterpret_cast<const float2*>(o - CW);
+    const float2 o2 = *reinterpret_cast<const float2*>(o);
+    // far end of the chain, kept inside the column's colour array (a clamped word is unused)
+    const float ox = o[kp ? ((vb & BT_CL) ? 1 : 2) : ((vb & BT_CL) ? 0 : -1)];
+    const float2 r2 = *reinterpret_cast<const float2*>(ce + 2 * KK);
+    float pW0 = w2.x, pW1 = w2.y;
+    float pB0 = kp ? o2.x : ox;          // k - 1 of the first cell
+    const float pTB = kp ? o2.y : o2.x;  // k + 1 of the first = k - 1 of the second
+    const float pT1 = kp ? ox : o2.y;
+    if (PRESS) {
+      if (ci & (1u << 29)) {  // physical west: p[0] -> p[1]
+        pW0 = c2.x;
+        pW1 = c2.y;
+      }
+      if (kp && (d.w & BT_BOT)) pB0 = c2.x;  // bottom: p[.,.,0] -> p[.,.,1]
+    }
+    // sor.py:164-171: E, W, N, S, T, B summed left to right
+    float nb0 = a.w2l * e2.x, nb1 = a.w2l * e2.y;
+    nb0 = nb0 + a.w2s * pW0;
+    nb1 = nb1 + a.w2s * pW1;
+    nb0 = nb0 + a.w3l * n2.x;
+    nb1 = nb1 + a.w3l * n2.y;
+    nb0 = nb0 + a.w3s * s2.x;
+    nb1 = nb1 + a.w3s * s2.y;
+    nb0 = nb0 + a.w4l * pTB;
+    nb1 = nb1 + a.w4l * pT1;
+    nb0 = nb0 + a.w4s * pB0;
+    nb1 = nb1 + a.w4s * pTB;
+    // sor.py:197: reltmp = omega * (cn1 * (nb - rhs) - p)
+    const float rel0 = a.om * (a.cn1 * (nb0 - r2.x) - c2.x);
+    const float rel1 = a.om * (a.cn1 * (nb1 - r2.y) - c2.y);
+    const float np0 = v0 ? c2.x + rel0 : c2.x;
+    const float np1 = v1 ? c2.y + rel1 : c2.y;
+    *reinterpret_cast<float2*>(ce) = make_float2(np0, np1);  // (an unused slot keeps its value)
+    const unsigned long long w0 = tagw | __float_as_uint(np0), w1 = tagw | __float_as_uint(np1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = h ? d.z : d.y;  // a column lies on at most two faces
+      if (v < 0) continue;
+      if (!SLAB) {
+        st_ll_pair(X + (unsigned)v, w0, w1);
+      } else {
+        const unsigned fo = (unsigned)(v & PUB_OFF);
+        if (v & PUB_RW) st_ll_pair_sys(XRw + fo, w0, w1);
+        else if (v & PUB_RE) st_ll_pair_sys(XRe + fo, w0, w1);
+        else st_ll_pair(X + fo, w0, w1);
+      }
+    }
+    if (v0) acc += (double)rel0 * (double)rel0;
+    if (v1) acc += (double)rel1 * (double)rel1;
+  }
   return acc;
 }
 
@@ -579,6 +683,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   unsigned* coltab = reinterpret_cast<unsigned*>(smem + ((s_floats + 3) & ~3LL));   // [TI*TJ]
   int2* pubcol = reinterpret_cast<int2*>(coltab + ((pl.ti_max * pl.tj_max + 3) & ~3)); // [TI*TJ]
   int4* rcvtab = reinterpret_cast<int4*>(pubcol + ((pl.ti_max * pl.tj_max + 1) & ~1));  // [2TI+2TJ]
+  int4* btab = rcvtab + 2 * (pl.ti_max + pl.tj_max);  // [boundary units] (RES_BTAB)
   const long long fstride = pl.fstride;
   const long long tstride = 4 * fstride;     // words per tile in one face buffer
   const long long bstride = pl.bstride;      // words per face buffer (tiles, then 2 nj ghost slots)
@@ -697,6 +802,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (tx && tid == 0) tx[6] = gtimer();
+#if RES_BTAB
+  // boundary-unit table: each thread writes the entries it will walk
+  const int nbu = nbnd * (KKF >> 1);
+  for (int w = tid; w < nbu; w += nth) {
+    const int c = w / (KKF >> 1);
+    btab[w] = btab_entry(coltab[c], pubcol[c], w - c * (KKF >> 1), KK, km);
+  }
+#endif
 
   // tags: pass n of this launch is tag0 + n + 2; *epoch advances by the tags
   // a launch uses, so tags never repeat across launches and stale words can
@@ -722,7 +835,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
   const int ig0 = iu0 / nint1, icc0 = iu0 - ig0 * nint1;
   const int idg = nth / nint1, idcc = nth - idg * nint1;
   const int HPb = KKF >> 1;
+#if !RES_BTAB
   const int bc0 = tid / HPb, bj0 = tid - bc0 * HPb, bdq = nth / HPb, bdr = nth - bdq * HPb;
+#endif
   // receive walk over slot PAIRS (face column q, slots sl, sl + 1; sl even):
   // pair w = tid + nth u, one 16-byte load each (two LL words).  The first
   // RCVP pairs of every thread keep their descriptors in registers for the
@@ -860,8 +975,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
     unsigned long long* XRw = pw ? a.peer_w + (n & 3) * bstride + ghost_e : nullptr;  // west peer's ghost-E slot tj
     unsigned long long* XRe = pe ? a.peer_e + (n & 3) * bstride + ghost_w : nullptr;  // east peer's ghost-W slot tj
     if (!RES_DBG(a, 2))
+#if RES_BTAB
+      acc += update_boundary_tab<PRESS, SLAB>(a, S, btab, nbu, X, XRw, XRe, tag, nrd, KK, CW, sI);
+#else
       acc += update_boundary<PRESS, SLAB>(a, S, coltab, pubcol, X, XRw, XRe, tag, bc0, bj0, bdq, bdr, nbnd, HPb, nrd,
                                          KK, CW, sI, km);
+#endif
     if (tr && tid == 0) tr[NST * n + 2] = tr[NST * n + 3] = tr[NST * n + 4] = gtimer();
     if (!RES_DBG(a, 2))
       acc += update_phase<PRESS>(a, S, coltab, nbnd, ncol, nseg_i, ig0, icc0, inu, idg, idcc, L_i, KTI, nrd, KK, CW, sI,
@@ -964,7 +1083,10 @@ static size_t plan_smem(int tim, int tjm, int kk) {
   const size_t coltab = 4ull * ((tim * tjm + 3) & ~3);
   const size_t pubcol = 8ull * ((tim * tjm + 1) & ~1);
   const size_t rcvtab = 16ull * 2 * (tim + tjm);
-  return arrays + coltab + pubcol + rcvtab;
+    // boundary-unit table: every column of a tile up to 3 x 3, else the ring
+  const int nb = (tim <= 2 || tjm <= 2) ? tim * tjm : 2 * tjm + 2 * (tim - 2);
+  const size_t btab = RES_BTAB ? 16ull * nb * (((kk + 1) & ~1) >> 1) : 0;
+  return arrays + coltab + pubcol + rcvtab + btab;
 }
 
 // Shared-memory bank load of the interior runs for a row pad: warps of 32
