@@ -302,19 +302,20 @@ __global__ void __launch_bounds__(PH_WARPS * 32) k_press_halo_rows(Geo g, const 
 // residuals[it] = (sum of pass-0 partials) + (sum of pass-1 partials), each
 // summed by one fixed-order tree (deterministic; numpy's pairwise order is
 // matched only to rtol ~1e-15).
-__global__ void k_reduce_res(const double* __restrict__ partials, int nblk, double* __restrict__ out) {
-  __shared__ double red[8];
+// res[it]: both passes' partials of iteration it ([2][nblk], contiguous) in
+// one fixed-order block reduction (1024 threads: the rows are short, so the
+// reduction is load-latency bound and wants every load in flight at once)
+constexpr int RES_RED_THREADS = 1024;
+__global__ void __launch_bounds__(RES_RED_THREADS) k_reduce_res(const double* __restrict__ partials, int nblk,
+                                                                 double* __restrict__ out) {
+  __shared__ double red[RES_RED_THREADS / 32];
   const int it = blockIdx.x;
-  double tot = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const double* q = partials + ((long long)it * 2 + pass) * nblk;
-    double a = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) a += q[b];
-    a = block_sum<8>(a, red);
-    __syncthreads();
-    if (threadIdx.x == 0) tot += a;
-  }
-  if (threadIdx.x == 0) out[it] = tot;
+  const double* q = partials + (long long)it * 2 * nblk;
+  double a = 0.0;
+#pragma unroll 4
+  for (int b = threadIdx.x; b < 2 * nblk; b += RES_RED_THREADS) a += q[b];
+  a = block_sum<RES_RED_THREADS / 32>(a, red);
+  if (threadIdx.x == 0) out[it] = a;
 }
 
 // ---------------------------------------------------------------------------
@@ -417,12 +418,12 @@ int reduce_scratch(int nblk, int n_iter) {
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st) {
   const int nch = (nblk + RED_CHUNK - 1) / RED_CHUNK;
   if (nch <= 1) {
-    k_reduce_res<<<n_iter, 256, 0, st>>>(partials, nblk, out);
+    k_reduce_res<<<n_iter, RES_RED_THREADS, 0, st>>>(partials, nblk, out);
     return;
   }
   double* scratch = const_cast<double*>(partials) + (long long)2 * n_iter * nblk;
   k_reduce_chunks<<<dim3(nch, 2 * n_iter), 256, 0, st>>>(partials, nblk, nch, scratch);
-  k_reduce_res<<<n_iter, 256, 0, st>>>(scratch, nch, out);
+  k_reduce_res<<<n_iter, RES_RED_THREADS, 0, st>>>(scratch, nch, out);
 }
 
 int sor_kernels_per_solve(const Geo& g, const SorC& cf, int n_iter, int scheme, int policy, bool resident,

@@ -128,6 +128,48 @@ __global__ void __launch_bounds__(256) k_split_pack(Geo g, SplitGeo sg, const fl
   }
 }
 
+// k_split_pack with four cells of a row per thread (16-byte loads, 8-byte
+// stores into each colour array): rows of km + 2 = 4q words start 16-byte
+// aligned and a group's four cells are two consecutive slots of each colour.
+// Same per-cell rules as k_split_pack.
+template <int POL, bool COPY>
+__global__ void __launch_bounds__(256) k_split_pack4(Geo g, SplitGeo sg, const float* __restrict__ p,
+                                                     const float* __restrict__ rhs, float* __restrict__ ps,
+                                                     float* __restrict__ rs, float* __restrict__ ps2) {
+  const int G = (g.km + 2) >> 2;  // groups per row
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  if (t >= nrow * G) return;
+  const long long row = t / G;
+  const int k0 = 4 * (int)(t - row * G);
+  const int i = (int)(row / (g.jm + 2)), j = (int)(row - (long long)i * (g.jm + 2));
+  const int par = (i + g.ioff + j + 1) & 1;
+  const bool rowhalo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1;
+  const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+  const bool remap = POL == 1 && !foreign;
+  const bool zero_row = remap && i == g.im + 1;
+  const int ii = (remap && i == 0) ? 1 : i;
+  const int jj = (remap && rowhalo) ? (j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j)) : j;
+  const float4 P = *reinterpret_cast<const float4*>(p + ((long long)ii * (g.jm + 2) + jj) * (g.km + 2) + k0);
+  const float4 R = *reinterpret_cast<const float4*>(rhs + row * (g.km + 2) + k0);
+  float v[4] = {P.x, P.y, P.z, P.w};
+  if (remap && k0 == 0) v[0] = P.y;  // p[0] -> p[1]
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (zero_row || (remap && k0 + e == g.km + 1)) v[e] = 0.0f;
+  const int c0 = (par + k0) & 1;
+  const long long d0 = (long long)c0 * sg.n + row * sg.khp + (k0 >> 1);
+  const long long d1 = (long long)(1 - c0) * sg.n + row * sg.khp + (k0 >> 1);
+  *reinterpret_cast<float2*>(ps + d0) = make_float2(v[0], v[2]);
+  *reinterpret_cast<float2*>(ps + d1) = make_float2(v[1], v[3]);
+  *reinterpret_cast<float2*>(rs + d0) = make_float2(R.x, R.z);
+  *reinterpret_cast<float2*>(rs + d1) = make_float2(R.y, R.w);
+  if (COPY) {
+    *reinterpret_cast<float2*>(ps2 + d0) = make_float2(v[0], v[2]);
+    *reinterpret_cast<float2*>(ps2 + d1) = make_float2(v[1], v[3]);
+  }
+}
+
 // Pass loads go through the read-only (non-coherent) path: within a pass the
 // only locations written besides the thread's own cells are the PRESS
 // mirror slots, each read earlier in the pass by the thread that writes it.
@@ -674,12 +716,58 @@ __global__ void __launch_bounds__(256) k_split_unpack(Geo g, SplitGeo sg, const 
   if (flags) flag_or(flags, bits);
 }
 
+// k_split_unpack with four cells of a row per thread (see k_split_pack4)
+template <int POL>
+__global__ void __launch_bounds__(256) k_split_unpack4(Geo g, SplitGeo sg, const float* __restrict__ ps,
+                                                       float* __restrict__ p, unsigned* flags) {
+  const int G = (g.km + 2) >> 2;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  unsigned bits = 0;
+  if (t < nrow * G) {
+    const long long row = t / G;
+    const int k0 = 4 * (int)(t - row * G);
+    const int i = (int)(row / (g.jm + 2)), j = (int)(row - (long long)i * (g.jm + 2));
+    const bool rowhalo = i == 0 || i == g.im + 1 || j == 0 || j == g.jm + 1;
+    const bool foreign = (i == 0 && !g.west_bc) || (i == g.im + 1 && !g.east_bc);
+    const bool remap = POL == 1 && !foreign;
+    const bool zero_row = remap && i == g.im + 1;
+    const int ii = (remap && i == 0) ? 1 : i;
+    const int jj = (remap && rowhalo) ? (j == 0 ? g.jm : (j == g.jm + 1 ? 1 : j)) : j;
+    const int par = (ii + g.ioff + jj + 1) & 1;
+    const long long sb = ((long long)ii * (g.jm + 2) + jj) * sg.khp + (k0 >> 1);
+    const int c0 = (par + k0) & 1;
+    const float2 A = *reinterpret_cast<const float2*>(ps + (long long)c0 * sg.n + sb);        // k0, k0 + 2
+    const float2 B = *reinterpret_cast<const float2*>(ps + (long long)(1 - c0) * sg.n + sb);  // k0 + 1, k0 + 3
+    float v[4] = {A.x, B.x, A.y, B.y};
+    if (remap && k0 == 0) v[0] = B.x;  // p[0] -> p[1]
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (zero_row || (remap && k0 + e == g.km + 1)) v[e] = 0.0f;
+      if (flags && !finite32(v[e])) bits = F_PRESS;
+    }
+    *reinterpret_cast<float4*>(p + row * (g.km + 2) + k0) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  if (flags) flag_or(flags, bits);
+}
+
 }  // namespace
 
 void launch_split_pack(const Geo& g, const float* p, const float* rhs, float* split, int policy, cudaStream_t st,
                        float* p_copy) {
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  if (((g.km + 2) & 3) == 0) {  // 16-byte row groups
+    const unsigned nb4 = (unsigned)((nrow * ((g.km + 2) >> 2) + 255) / 256);
+    if (p_copy) {
+      if (policy == 1) k_split_pack4<1, true><<<nb4, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+      else k_split_pack4<0, true><<<nb4, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
+    } else {
+      if (policy == 1) k_split_pack4<1, false><<<nb4, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, nullptr);
+      else k_split_pack4<0, false><<<nb4, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, nullptr);
+    }
+    return;
+  }
   const unsigned nb = (unsigned)((nrow + 7) / 8);
   if (p_copy) {
     if (policy == 1) k_split_pack<1, true><<<nb, 256, 0, st>>>(g, sg, p, rhs, split, split + 2 * sg.n, p_copy);
@@ -888,6 +976,12 @@ void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* r
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st) {
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
+  if (((g.km + 2) & 3) == 0) {  // 16-byte row groups
+    const unsigned nb4 = (unsigned)((nrow * ((g.km + 2) >> 2) + 255) / 256);
+    if (policy == 1) k_split_unpack4<1><<<nb4, 256, 0, st>>>(g, sg, split, p, flags);
+    else k_split_unpack4<0><<<nb4, 256, 0, st>>>(g, sg, split, p, flags);
+    return;
+  }
   const unsigned nb = (unsigned)((nrow + 7) / 8);
   if (policy == 1) k_split_unpack<1><<<nb, 256, 0, st>>>(g, sg, split, p, flags);
   else k_split_unpack<0><<<nb, 256, 0, st>>>(g, sg, split, p, flags);
