@@ -309,6 +309,7 @@ constexpr int RES_RED_THREADS = 1024;
 __global__ void __launch_bounds__(RES_RED_THREADS) k_reduce_res(const double* __restrict__ partials, int nblk,
                                                                  double* __restrict__ out) {
   __shared__ double red[RES_RED_THREADS / 32];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic launch: the partials are upstream output)
   const int it = blockIdx.x;
   const double* q = partials + (long long)it * 2 * nblk;
   double a = 0.0;
@@ -418,7 +419,17 @@ int reduce_scratch(int nblk, int n_iter) {
 void launch_reduce_res(const double* partials, int nblk, int n_iter, double* out, cudaStream_t st) {
   const int nch = (nblk + RED_CHUNK - 1) / RED_CHUNK;
   if (nch <= 1) {
-    k_reduce_res<<<n_iter, RES_RED_THREADS, 0, st>>>(partials, nblk, out);
+    static const bool pdl = !(std::getenv("LESB_PDL") && std::atoi(std::getenv("LESB_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_iter);
+    cfg.blockDim = dim3(RES_RED_THREADS);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_reduce_res, partials, nblk, out);
     return;
   }
   double* scratch = const_cast<double*>(partials) + (long long)2 * n_iter * nblk;

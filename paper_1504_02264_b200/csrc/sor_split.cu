@@ -52,6 +52,7 @@
 // sum += rel*rel term -- summed per thread in row/slot order, per block by a
 // fixed shuffle tree, per iteration by launch_reduce_res.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "lesb_common.cuh"
@@ -720,6 +721,9 @@ __global__ void __launch_bounds__(256) k_split_unpack(Geo g, SplitGeo sg, const 
 template <int POL>
 __global__ void __launch_bounds__(256) k_split_unpack4(Geo g, SplitGeo sg, const float* __restrict__ ps,
                                                        float* __restrict__ p, unsigned* flags) {
+  // programmatic dependent launch after the last pass
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int G = (g.km + 2) >> 2;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
@@ -805,7 +809,10 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
   static const int env_rpt = std::getenv("LESB_RBT_RPT") ? std::atoi(std::getenv("LESB_RBT_RPT")) : 0;
   const int rpt = 2;  // (4 rows per thread measured slower; RBT_RPT kept as a template parameter)
   (void)env_rpt;
-  int tr = env_tr > 0 ? env_tr : rpt * (512 / (2 * sg.kh4));
+  // ~144 threads per tile (24 rows at km = 90): measured across 150^2-600^2 x 90,
+  // both halo policies, against 16-60 rows (the old 42-row default was 6-15%
+  // slower at 300^2: its 2400 tiles leave a ninth round for 32 of 296 CTAs)
+  int tr = env_tr > 0 ? env_tr : rpt * std::max(1, 288 / (2 * sg.kh4));
   tr = std::max(rpt, tr - tr % rpt);
   while (tr > rpt && sg.kh4 * (tr / rpt) > 512) tr -= rpt;
   const size_t stage = (size_t)(5 * tr + 2) * sg.khp * sizeof(float);
@@ -834,6 +841,10 @@ static RbtPlan rbt_plan(const Geo& g, const SplitGeo& sg) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sor_rbt<1, 2, 1>, pl.threads, pl.smem);
   if (per < 1) per = 1;
   pl.grid = std::min(pl.ntiles, sms * per);
+  static const bool verbose = std::getenv("LESB_RBT_VERBOSE") != nullptr;
+  if (verbose)
+    std::fprintf(stderr, "rbt_plan im=%d jm=%d km=%d: tr=%d threads=%d smem=%zu per=%d grid=%d ntiles=%d\n", g.im, g.jm,
+                 g.km, pl.tr, pl.threads, pl.smem, per, pl.grid, pl.ntiles);
   return pl;
 }
 
@@ -976,10 +987,19 @@ void launch_tws_sweep(const Geo& g, const float* src, float* dst, const float* r
 void launch_split_unpack(const Geo& g, const float* split, float* p, int policy, unsigned* flags, cudaStream_t st) {
   const SplitGeo sg = split_geo(g);
   const long long nrow = (long long)(g.im + 2) * (g.jm + 2);
-  if (((g.km + 2) & 3) == 0) {  // 16-byte row groups
-    const unsigned nb4 = (unsigned)((nrow * ((g.km + 2) >> 2) + 255) / 256);
-    if (policy == 1) k_split_unpack4<1><<<nb4, 256, 0, st>>>(g, sg, split, p, flags);
-    else k_split_unpack4<0><<<nb4, 256, 0, st>>>(g, sg, split, p, flags);
+  if (((g.km + 2) & 3) == 0) {  // 16-byte row groups, launched programmatically after the last pass
+    static const bool pdl = !(std::getenv("LESB_PDL") && std::atoi(std::getenv("LESB_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((nrow * ((g.km + 2) >> 2) + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (policy == 1) cudaLaunchKernelEx(&cfg, k_split_unpack4<1>, g, sg, split, p, flags);
+    else cudaLaunchKernelEx(&cfg, k_split_unpack4<0>, g, sg, split, p, flags);
     return;
   }
   const unsigned nb = (unsigned)((nrow + 7) / 8);
