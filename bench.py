@@ -486,7 +486,10 @@ def run_gpu(args):
                               "frac": step_gbs / hbm, "peak_kind": peak_kind},
             "phase_ms": {"velnw_bondv1": phase_ms[0], "velfg_feedbf_les_adam_rhs": phase_ms[1],
                          "sor_passes": phase_ms[2], "halo_and_residuals": phase_ms[3]},
-            "roofline": {"kernel": f"{sor_kernel} (whole {N_ITER}-iteration red-black solve, one launch)",
+            "roofline": {"kernel": (f"{sor_kernel} (whole {N_ITER}-iteration red-black solve, one launch)"
+                                   if sor_kernel == "k_sor_resident" else
+                                   f"{sor_kernel} ({2 * N_ITER} colour-pass launches with the layout pack / unpack "
+                                   "and the residual reduction: the solve phase of the step)"),
                          "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": b_solve, "bytes_per_cell_iteration": B_ITER,
@@ -500,9 +503,47 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "wall_s": wall,
         }
+        if world == 1 and not args.grid and not args.no_extras:
+            line["extras"] = side_lines()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _last_json(cmd, timeout):
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    if r.returncode != 0 or not lines:
+        raise RuntimeError(f"exit {r.returncode}: {(r.stderr or r.stdout)[-300:]}")
+    return json.loads(lines[-1])
+
+
+def side_lines():
+    """The other BASELINE.json configurations that fit one GPU, measured after
+    the headline run by the same tools the profiles use, so that they land in
+    the driver's record: config 3 (press-only red-black solve, 512x512x90, the
+    HBM-bound case) and the 300x300x90 step (the per-GPU size of the weak
+    scaling runs).  Each in its own process; a failure is recorded, not raised."""
+    out = {}
+    try:
+        d = _last_json([sys.executable, os.path.join(ROOT, "scripts", "bench_press.py"), "512", "512", "90",
+                        "--path", "1", "--reps", "5"], 600)
+        out["config3_press_only_512x512x90"] = {
+            "kernel": d.get("sor_kernel"), "us_per_iteration": d["us_per_iteration"],
+            "roofline_frac_12B": d["roofline"]["frac"], "achieved_gbs": d["roofline"]["achieved_gbs"],
+            "halo": "stored", "n_iter": 50, "timing": "median of 5 device-timed solves, inputs resident"}
+    except Exception as e:  # noqa: BLE001
+        out["config3_press_only_512x512x90"] = {"error": str(e)[:300]}
+    try:
+        d = _last_json([sys.executable, os.path.abspath(__file__), "--grid", "300", "300", "90", "--steps", "20",
+                        "--warmup", "5", "--no-cpu", "--no-e2e", "--no-extras"], 600)
+        out["step_300x300x90"] = {"steps_per_s": d["value"], "ms_per_step": d["ms_per_step"],
+                                  "step_roofline_frac": d["step_roofline"]["frac"],
+                                  "sor_kernel": d["roofline"]["kernel"], "sor_roofline_frac": d["roofline"]["frac"],
+                                  "clocks": d.get("clocks")}
+    except Exception as e:  # noqa: BLE001
+        out["step_300x300x90"] = {"error": str(e)[:300]}
+    return out
 
 
 def e2e_run(P, N, gi, torch, grid, st0, inflow, args):
@@ -573,6 +614,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e measurement (profiling runs)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the side lines (config 3 press-only at 512^2, the 300^2 step) measured after the run")
     ap.add_argument("--grid", type=int, nargs=3, metavar=("IM", "JM", "KM"),
                     help="another grid (per GPU) with config 2's buildings scaled to it; default config 2")
     args = ap.parse_args()

@@ -17,7 +17,7 @@ timeout 300 python scripts/bench_press.py 512 512 90 --path 1 --reps 5 --halo pr
 timeout 300 python scripts/bench_press.py 512 512 90 --path 3 --reps 3 >> gpurun_out/ev/press.jsonl
 timeout 600 python scripts/bench_press.py 512 512 90 --scheme twinned --reps 3 --cpu >> gpurun_out/ev/press.jsonl
 python scripts/res_trace.py > gpurun_out/ev/res_trace.txt 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/ev/launches.csv python bench.py --steps 6 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_resident|k_fused_rhs|k_velnw_bondv1" -s 3 -c 3 -o gpurun_out/ev/step_full python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/ev/ncu_step.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/ev/launches.csv python bench.py --steps 6 --warmup 3 --no-cpu --no-e2e --no-extras > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_resident|k_fused_rhs|k_velnw_bondv1" -s 3 -c 3 -o gpurun_out/ev/step_full python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-extras > gpurun_out/ev/ncu_step.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sor_rbt" -s 10 -c 2 -o gpurun_out/ev/rbt512_full python scripts/bench_press.py 512 512 90 --path 1 --reps 1 --n-iter 6 > gpurun_out/ev/ncu_rbt512.log 2>&1
 ls -la gpurun_out/ev
