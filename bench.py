@@ -13,13 +13,14 @@ Arms
                the domain stream, L2 flushed (256 MB write) before every
                timed step.  The reference dynamics blow up at step 19 with
                buildings, so the state is re-initialised
-               (untimed device copy) every 8 steps; kernel cost is
+               (untimed device copy) every 16 steps; kernel cost is
                data-independent.
                `e2e` = the same steps through the public Python API
                (les.step on a FlowState), timed on the host clock per
-               8-step window that uploads the initial state from pinned host
-               memory, runs 8 steps (inflow H2D, stage flags + residual
-               history D2H per step) and downloads the six fields.
+               16-step window (the longest that stays below the blow-up)
+               that uploads the initial state from pinned host memory, runs
+               16 steps (inflow H2D, stage flags + residual history D2H per
+               step) and downloads the six fields.
   reference    the reference on the host CPU: the unmodified gmcf_mini.les.step
                from baseline/_ref (scripts/install_reference.sh; the numpy
                port in oracle/ only when that is absent), a bounded sample
@@ -53,7 +54,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 METRIC = "LES time steps/sec and MLUPS at 1/2/4/8 B200; % of HBM-bandwidth roofline"
 IM, JM, KM = 150, 150, 90
 N_ITER = 50
-REINIT = 8
+REINIT = 16  # steps per state window (config 2 blows up at step 19)
 B_ITER = 12                     # SOR RB iteration, cn1 a scalar: p read + p write + rhs read
 B_STEP = 216 + B_ITER * N_ITER  # algorithmic bytes / interior cell / step: 816 (SURVEY 8(d), cn1 scalarised)
 WORKLOAD = "config2: 150x150x90, h=2, dt=0.5, 3x3 buildings, log-law inflow, RB SOR 50 iters"
