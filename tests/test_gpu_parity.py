@@ -198,6 +198,29 @@ def test_step_against_oracle_odd_shapes(P):
                 assert bits_equal(getattr(fs, n), getattr(o, n)), ((im, jm, km), scheme, s, n)
 
 
+@pytest.mark.parametrize("dims", [(10, 7, 10), (6, 9, 14), (5, 5, 2), (7, 11, 30)])
+def test_sor_pitch4_odd_jm_against_oracle(P, dims):
+    """Column pitches km + 2 divisible by 4 (the colour-split layout's
+    16-byte pack / unpack, sor_split.cu k_split_pack4 / k_split_unpack4) with
+    odd jm (the press policy's periodic halo rows take the other colour):
+    both schemes and both halo policies, bitwise against the oracle's
+    solve_pressure; residuals to 1e-12."""
+    from oracle import les_oracle as O
+
+    im, jm, km = dims
+    p0, rhs = gi.sor_problem(im, jm, km, seed=im * 97 + jm * 13 + km)
+    grid = P.Grid.uniform(im, jm, km, 2.0)
+    c = P.sor.build_uniform_coeffs(grid)
+    oc = O.uniform_coeffs(im, jm, km, 2.0)
+    halo = P.les._pressure_halo(grid)
+    for scheme, om in ((P.Scheme.REDBLACK, 1.7), (P.Scheme.TWINNED, 1.0)):
+        for pol, fn in (("stored", None), ("press", halo)):
+            p, res = P.sor.solve_pressure(p0.copy(), rhs, c, om, 7, scheme, 1, halo_fn=fn)
+            po, reso = O.solve_pressure(p0, rhs, oc, om, 7, scheme.value, None if pol == "stored" else "press")
+            assert bits_equal(p, po), (dims, scheme, pol)
+            np.testing.assert_allclose(res, reso, rtol=RTOL_RES, atol=0)
+
+
 @pytest.mark.parametrize("dims", [(36, 36, 600), (48, 40, 400), (30, 74, 257)])
 def test_deep_columns_against_oracle(P, dims, request):
     """Deep columns on grids the resident solver takes: 3x3-class tiles of
