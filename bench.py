@@ -528,7 +528,7 @@ def side_lines():
     out = {}
     try:
         d = _last_json([sys.executable, os.path.join(ROOT, "scripts", "bench_press.py"), "512", "512", "90",
-                        "--path", "1", "--reps", "5"], 600)
+                        "--path", "1", "--reps", "5"], 300)
         out["config3_press_only_512x512x90"] = {
             "kernel": d.get("sor_kernel"), "us_per_iteration": d["us_per_iteration"],
             "roofline_frac_12B": d["roofline"]["frac"], "achieved_gbs": d["roofline"]["achieved_gbs"],
@@ -537,7 +537,7 @@ def side_lines():
         out["config3_press_only_512x512x90"] = {"error": str(e)[:300]}
     try:
         d = _last_json([sys.executable, os.path.abspath(__file__), "--grid", "300", "300", "90", "--steps", "20",
-                        "--warmup", "5", "--no-cpu", "--no-e2e", "--no-extras"], 600)
+                        "--warmup", "5", "--no-cpu", "--no-e2e", "--no-extras"], 300)
         out["step_300x300x90"] = {"steps_per_s": d["value"], "ms_per_step": d["ms_per_step"],
                                   "step_roofline_frac": d["step_roofline"]["frac"],
                                   "sor_kernel": d["roofline"]["kernel"], "sor_roofline_frac": d["roofline"]["frac"],
