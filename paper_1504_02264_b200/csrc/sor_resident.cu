@@ -13,19 +13,21 @@
 //       16-byte load per slot pair, issued during pass n-1's interior runs)
 //       into this tile's halo columns; barrier
 //     update the colour-nrd cells of the tile's BOUNDARY columns, two slots
-//       per work unit, publishing each pair of new values with one 16-byte
-//       store into the tile's face slots (or, on an x-slab edge, straight
-//       into the neighbour slab's ghost slot -- NVLink peer memory across GPUs)
-//     update the colour-nrd cells of the tile's INTERIOR columns while the
-//       published faces travel
+//       per work unit (decoded once per solve into a per-unit table),
+//       publishing each pair of new values with one 16-byte store into the
+//       tile's face slots (or, on an x-slab edge, straight into the neighbour
+//       slab's ghost slot -- NVLink peer memory across GPUs)
+//     update the colour-nrd cells of the tile's INTERIOR columns, in runs of
+//       slot pairs, while the published faces travel
 //
 // Layout ("colour split"): cell (i,j,k) lives in colour array
 // colour(i,j,k) = (i+j+k+1)&1 at slot k>>1 of its column, so for a fixed
-// column the colour-c cells are consecutive slots and a warp's lanes touch
-// consecutive words for the centre, all six neighbours and rhs.  With
-// kp = parity of the colour's k values in the column and t = 0,1,...:
-//   k = 2t + 2 - kp, centre slot t + 1 - kp, top slot t + 1, bottom slot t,
-// so every address is (column base + t + constant).
+// column the colour-c cells are consecutive slots: slot s of the colour-nrd
+// array holds k = 2 s + kp (kp the parity of the colour's k values in the
+// column), its E/W/N/S neighbours sit at slot s of the neighbour columns'
+// other-colour arrays and its top/bottom at slots s + kp, s + kp - 1 of its
+// own column's other-colour array.  A warp's lanes work on the same slot
+// pair of consecutive columns (64-bit shared accesses at one offset).
 //
 // Work units are walked with an incremental decode (no integer division in
 // the pass loop) over a column table whose boundary columns come first.  Halo slots take the colour of their storage position; for the
