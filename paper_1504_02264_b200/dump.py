@@ -80,3 +80,55 @@ def write_state(state, out_dir, names=("u", "v", "w", "p")) -> list:
         write_field(p, getattr(state, n))
         paths.append(p)
     return paths
+
+
+# Checkpoint / resume (the reference has final dumps only).  A step
+# reads u, v, w, p, fgh, fgh_old and the mask; the GMCF format is 3-D, so the
+# two force fields are stored per component (``fgh.0.gmcf`` ...).
+CHECKPOINT_FIELDS = ("u", "v", "w", "p", "mask", "fgh", "fgh_old")
+_VECTOR_FIELDS = ("fgh", "fgh_old")
+
+
+def write_checkpoint(state, out_dir) -> list:
+    """Everything ``les.step`` reads from ``state`` as GMCF dumps plus a
+    sidecar listing them; ``read_checkpoint`` restores it and the run then
+    continues bitwise as if it had not stopped (tests/test_gpu_cli.py)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    paths, entries = [], {}
+    for n in CHECKPOINT_FIELDS:
+        arr = np.asarray(getattr(state, n))
+        if n in _VECTOR_FIELDS:
+            for m in range(arr.shape[-1]):
+                p = out / f"{n}.{m}.gmcf"
+                write_field(p, np.ascontiguousarray(arr[..., m]))
+                paths.append(p)
+                entries[f"{n}.{m}"] = p.name
+        else:
+            p = out / f"{n}.gmcf"
+            write_field(p, arr)
+            paths.append(p)
+            entries[n] = p.name
+    write_sidecar(out / "checkpoint.txt", entries)
+    return paths
+
+
+def read_checkpoint(state, in_dir) -> None:
+    """Load ``write_checkpoint``'s files into ``state`` (a FlowState of the same
+    grid: the shapes are checked); on the device state each field is uploaded
+    at the next step."""
+    src = Path(in_dir)
+    g = state.grid
+    shape = (g.im + 2, g.jm + 2, g.km + 2)
+    for n in CHECKPOINT_FIELDS:
+        if n in _VECTOR_FIELDS:
+            comps = [read_field(src / f"{n}.{m}.gmcf") for m in range(3)]
+            for c in comps:
+                if c.shape != shape:
+                    raise ValueError(f"{n}: checkpoint shape {c.shape} != state shape {shape}")
+            arr = np.stack(comps, axis=-1)
+        else:
+            arr = read_field(src / f"{n}.gmcf")
+            if arr.shape != shape:
+                raise ValueError(f"{n}: checkpoint shape {arr.shape} != state shape {shape}")
+        setattr(state, n, np.ascontiguousarray(arr, dtype=np.float32))

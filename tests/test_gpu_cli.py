@@ -179,3 +179,33 @@ def test_write_state_device_bytes_equal_reference_writer(tmp_path):
             rp = tmp_path / f"ref_{n}.gmcf"
             rdump.write_field(rp, getattr(o, n))
             assert rp.read_bytes() == path.read_bytes(), n
+
+
+def test_checkpoint_resume_bitwise(tmp_path):
+    """Checkpoint / resume of a device FlowState: 3 steps, write_checkpoint,
+    a fresh FlowState restored with read_checkpoint, 3 more steps -- bitwise
+    equal to 6 uninterrupted steps (the reference has final dumps only; this
+    is the resume half SURVEY 5 lists)."""
+    import paper_1504_02264_b200 as P
+
+    st = gi.config1_state()
+    g = P.Grid(32, 32, 16, st["dx1"], st["dy1"], st["dzn"])
+    inflow = P.WindProfile(*gi.default_inflow(16))
+
+    def fresh():
+        fs = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+        for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask"):
+            getattr(fs, n)[...] = st[n]
+        return fs
+
+    straight = fresh()
+    P.les.run_steps(straight, inflow, 6)
+    first = fresh()
+    P.les.run_steps(first, inflow, 3)
+    P.dump.write_checkpoint(first, tmp_path / "ck")
+    resumed = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    P.dump.read_checkpoint(resumed, tmp_path / "ck")
+    P.les.run_steps(resumed, inflow, 3)
+    for n in ("u", "v", "w", "fgh", "fgh_old", "p"):
+        a, b = getattr(straight, n), getattr(resumed, n)
+        assert np.array_equal(np.ascontiguousarray(a).view(np.uint32), np.ascontiguousarray(b).view(np.uint32)), n
