@@ -21,6 +21,20 @@
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
 
+#include <nvtx3/nvToolsExt.h>
+
+namespace {
+// NVTX range around a C ABI entry point (tracing): shows the
+// host-side step / solve calls in Nsight Systems; without a tool attached the
+// calls are no-ops.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
+
 using namespace lesb;
 
 namespace {
@@ -880,6 +894,7 @@ int lesb_strain_magnitude(lesb_handle h, float* out_host) {
 }
 
 int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* residuals_out) {
+  NvtxRange nvtx_range_("lesb_press");
   int rc = check_args_step(h, n_iter, scheme);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(h->mu);
@@ -902,6 +917,7 @@ int lesb_press(lesb_handle h, int n_iter, int scheme, float omega, double* resid
 }
 
 int lesb_sor_solve(lesb_handle h, int n_iter, int scheme, float omega, int halo_policy, double* residuals_out) {
+  NvtxRange nvtx_range_("lesb_sor_solve");
   int rc = check_args_step(h, n_iter, scheme);
   if (rc) return rc;
   if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
@@ -934,6 +950,7 @@ int lesb_sor_solve(lesb_handle h, int n_iter, int scheme, float omega, int halo_
 // ---- the time step ----
 int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* in_w, int n_iter, int scheme,
               float omega, double* residuals_out, int* fail_stage) {
+  NvtxRange nvtx_range_("lesb_step");
   int rc = check_args_step(h, n_iter, scheme);
   if (rc) return rc;
   if (!in_u || !in_v || !in_w) return fail(LESB_E_ARG, "inflow arrays are required");
@@ -986,6 +1003,7 @@ int lesb_set_inflow(lesb_handle h, const float* in_u, const float* in_v, const f
 }
 
 int lesb_step_async(lesb_handle h, int n_iter, int scheme, float omega) {
+  NvtxRange nvtx_range_("lesb_step_async");
   int rc = check_args_step(h, n_iter, scheme);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(h->mu);
@@ -1026,6 +1044,7 @@ int lesb_poll_failure(lesb_handle h, int* steps_done, int* fail_step, int* fail_
 
 int lesb_run_steps(lesb_handle h, int n_steps, const float* inflow, int n_profiles, int n_iter, int scheme,
                    float omega, int* steps_done, int* fail_stage) {
+  NvtxRange nvtx_range_("lesb_run_steps");
   if (!h || !inflow || n_profiles < 1 || n_steps < 0) return fail(LESB_E_ARG, "bad argument");
   int rc = check_args_step(h, n_iter, scheme);
   if (rc) return rc;
@@ -1205,6 +1224,7 @@ extern "C" {
 int lesb_solve_pressure(int im, int jm, int km, const float* p0, const float* rhs, const lesb_coeffs* c,
                         float omega, int n_iter, int scheme, int halo_policy, float* p_out, double* residuals,
                         int device) {
+  NvtxRange nvtx_range_("lesb_solve_pressure");
   if (n_iter < 1) return fail(LESB_E_ARG, "n_iter must be >= 1");
   if (scheme != LESB_REDBLACK && scheme != LESB_TWINNED) return fail(LESB_E_ARG, "unknown scheme");
   if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
@@ -1494,6 +1514,7 @@ static int group_sor(lesb_domain** hs, int n, int n_iter, int scheme, float omeg
 // over slabs in order) agree to summation-order tolerance.
 int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v, const float* in_w, int n_iter,
                     int scheme, float omega, double* residuals_out, int* fail_stage) {
+  NvtxRange nvtx_range_("lesb_group_step");
   if (!hs || n < 1 || !in_u || !in_v || !in_w) return fail(LESB_E_ARG, "bad argument");
   for (int s = 0; s < n; ++s) {
     int rc = check_args_step(hs[s], n_iter, scheme);
@@ -1553,6 +1574,7 @@ int lesb_group_step(lesb_handle* hs, int n, const float* in_u, const float* in_v
 // history is the sum of the slabs' histories, in slab order.
 int lesb_group_sor_solve(lesb_handle* hs, int n, int n_iter, int scheme, float omega, int halo_policy,
                          double* residuals_out) {
+  NvtxRange nvtx_range_("lesb_group_sor_solve");
   if (!hs || n < 1) return fail(LESB_E_ARG, "bad argument");
   if (halo_policy != LESB_HALO_STORED && halo_policy != LESB_HALO_PRESS) return fail(LESB_E_ARG, "unknown halo policy");
   for (int s = 0; s < n; ++s) {
