@@ -198,7 +198,7 @@ def test_step_against_oracle_odd_shapes(P):
                 assert bits_equal(getattr(fs, n), getattr(o, n)), ((im, jm, km), scheme, s, n)
 
 
-@pytest.mark.parametrize("dims", [(10, 7, 10), (6, 9, 14), (5, 5, 2), (7, 11, 30)])
+@pytest.mark.parametrize("dims", [(10, 7, 10), (6, 9, 14), (5, 5, 2), (7, 11, 30), (8, 7, 598)])
 def test_sor_pitch4_odd_jm_against_oracle(P, dims):
     """Column pitches km + 2 divisible by 4 (the colour-split layout's
     16-byte pack / unpack, sor_split.cu k_split_pack4 / k_split_unpack4) with
