@@ -1,0 +1,163 @@
+// Runtime-specialised step kernels.
+//
+// k_velnw_bondv1 and k_fused_rhs take the domain geometry as launch
+// parameters, so every neighbour address is a 64-bit multiply-add on runtime
+// strides; with the geometry as compile-time constants the offsets fold into
+// the load instructions (measured at 150x150x90: the fused kernel 62.5 ->
+// 57.5 us).  For domains of at least LESB_JIT_MIN_CELLS interior cells
+// (default 2^20) this file compiles the two kernels once per geometry with
+// NVRTC from the same device source the ahead-of-time build uses
+// (stages_dev.cuh, embedded by build.py as jit_src.inc), with the same
+// floating-point flags (-fmad=false, IEEE division and square root, no
+// flush to zero), so the specialised kernels are bitwise identical to the
+// ahead-of-time ones.  NVRTC is loaded with dlopen; if it is missing or a
+// compile fails the ahead-of-time kernels run (one message on stderr).
+// LESB_JIT=0 disables the specialisation.
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "lesb_common.cuh"
+#include "lesb_kernels.h"
+
+namespace lesb {
+namespace {
+
+#include "jit_src.inc"  // JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV
+
+struct Nvrtc {
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcAddNameExpression) add_name = nullptr;
+  decltype(&nvrtcGetLoweredName) lowered = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  bool ok = false;
+};
+
+Nvrtc load_nvrtc() {
+  Nvrtc n;
+  void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return n;
+#define SYM(f, name) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, name))
+  SYM(create, "nvrtcCreateProgram");
+  SYM(compile, "nvrtcCompileProgram");
+  SYM(log_size, "nvrtcGetProgramLogSize");
+  SYM(log, "nvrtcGetProgramLog");
+  SYM(cubin_size, "nvrtcGetCUBINSize");
+  SYM(cubin, "nvrtcGetCUBIN");
+  SYM(add_name, "nvrtcAddNameExpression");
+  SYM(lowered, "nvrtcGetLoweredName");
+  SYM(destroy, "nvrtcDestroyProgram");
+#undef SYM
+  n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.add_name && n.lowered &&
+         n.destroy;
+  return n;
+}
+
+const Nvrtc& nvrtc() {
+  static const Nvrtc n = load_nvrtc();
+  return n;
+}
+
+void warn_once(const std::string& what) {
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    std::fprintf(stderr, "liblesb200: runtime specialisation off (%s); the ahead-of-time kernels run\n",
+                 what.c_str());
+  });
+}
+
+cudaKernel_t compile(int kind, const Geo& g, int p2) {
+  const Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    warn_once("libnvrtc.so.12 not found");
+    return nullptr;
+  }
+  const std::string src = "#define LESB_JIT 1\n#define LESB_JIT_IM " + std::to_string(g.im) + "\n#define LESB_JIT_JM " +
+                          std::to_string(g.jm) + "\n#define LESB_JIT_KM " + std::to_string(g.km) +
+                          "\n#include \"stages_dev.cuh\"\n";
+  const char* headers[] = {JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV};
+  const char* names[] = {"lesb_common.cuh", "stages_dev.cuh"};
+  nvrtcProgram prog;
+  if (nv.create(&prog, src.c_str(), "lesb_jit.cu", 2, headers, names) != NVRTC_SUCCESS) {
+    warn_once("nvrtcCreateProgram failed");
+    return nullptr;
+  }
+  const std::string expr = kind == JIT_VELNW_BONDV1 ? (p2 ? "lesb::k_velnw_bondv1<true>" : "lesb::k_velnw_bondv1<false>")
+                                                    : (p2 ? "lesb::k_fused_rhs<true>" : "lesb::k_fused_rhs<false>");
+  nv.add_name(prog, expr.c_str());
+  // the ahead-of-time build's floating-point flags (build.py FLAGS)
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "--prec-div=true",
+                        "--prec-sqrt=true", "--ftz=false", "-lineinfo"};
+  const nvrtcResult rc = nv.compile(prog, sizeof(opts) / sizeof(opts[0]), opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) nv.log(prog, &log[0]);
+    nv.destroy(&prog);
+    warn_once("NVRTC compile failed: " + log.substr(0, 400));
+    return nullptr;
+  }
+  const char* lowered = nullptr;
+  nv.lowered(prog, expr.c_str(), &lowered);
+  const std::string sym = lowered ? lowered : "";
+  size_t nbin = 0;
+  nv.cubin_size(prog, &nbin);
+  std::vector<char> bin(nbin);
+  nv.cubin(prog, bin.data());
+  nv.destroy(&prog);
+  cudaLibrary_t lib;
+  if (sym.empty() || cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+    cudaGetLastError();
+    warn_once("cudaLibraryLoadData failed");
+    return nullptr;
+  }
+  cudaKernel_t k;
+  if (cudaLibraryGetKernel(&k, lib, sym.c_str()) != cudaSuccess) {
+    cudaGetLastError();
+    warn_once("cudaLibraryGetKernel failed");
+    return nullptr;
+  }
+  return k;
+}
+
+}  // namespace
+
+bool jit_enabled(const Geo& g) {
+  static const bool off = std::getenv("LESB_JIT") && std::atoi(std::getenv("LESB_JIT")) == 0;
+  static const long long min_cells =
+      std::getenv("LESB_JIT_MIN_CELLS") ? std::atoll(std::getenv("LESB_JIT_MIN_CELLS")) : (1LL << 20);
+  return !off && (long long)g.im * g.jm * g.km >= min_cells;
+}
+
+cudaKernel_t jit_stage_kernel(int kind, const Geo& g, int p2) {
+  if (!jit_enabled(g)) return nullptr;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int>, cudaKernel_t> cache;  // (kind, im, jm, km, p2)
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kind, g.im, g.jm, g.km, p2 ? 1 : 0);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  // a capture in progress must not see the compile's library load
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaKernel_t k = compile(kind, g, p2);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cache.emplace(key, k);  // (a failure is cached too: the ahead-of-time kernel from then on)
+  return k;
+}
+
+}  // namespace lesb

@@ -7,8 +7,10 @@
 // SURVEY Appendix B.
 #pragma once
 
+#ifndef __CUDACC_RTC__  // (NVRTC, jit.cu: the device types are built in)
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace lesb {
 

@@ -111,6 +111,13 @@ void launch_fused_rhs(const Geo& g, const Spac& s, const float* ub, const float*
                       cudaStream_t st);
 void launch_check_finite(const float* a, long long n, unsigned* flags, unsigned bit, cudaStream_t st);
 
+// Runtime-specialised step kernels (jit.cu): the kernel compiled with this
+// geometry as constants, or nullptr (small domain, LESB_JIT=0, no NVRTC) --
+// then the ahead-of-time kernel runs.
+enum { JIT_VELNW_BONDV1 = 0, JIT_FUSED_RHS = 1 };
+bool jit_enabled(const Geo& g);
+cudaKernel_t jit_stage_kernel(int kind, const Geo& g, int p2);
+
 // sor.cu
 int sor_blocks_rb(const Geo& g);
 int sor_blocks_tw(const Geo& g);
