@@ -26,11 +26,12 @@
 
 #include "lesb_common.cuh"
 #include "lesb_kernels.h"
+#include "sor_resident_dev.cuh"  // (ResPlan)
 
 namespace lesb {
 namespace {
 
-#include "jit_src.inc"  // JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV
+#include "jit_src.inc"  // JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV, JIT_SRC_RESIDENT_DEV
 
 struct Nvrtc {
   decltype(&nvrtcCreateProgram) create = nullptr;
@@ -79,28 +80,33 @@ void warn_once(const std::string& what) {
   });
 }
 
-cudaKernel_t compile(int kind, const Geo& g, int p2) {
+std::string geo_defines(const Geo& g) {
+  return "#define LESB_JIT 1\n#define LESB_JIT_IM " + std::to_string(g.im) + "\n#define LESB_JIT_JM " +
+         std::to_string(g.jm) + "\n#define LESB_JIT_KM " + std::to_string(g.km) + "\n";
+}
+
+// one kernel of `src` (which includes the embedded headers), by its name
+// expression; nullptr on any failure
+cudaKernel_t compile(const std::string& src, const std::string& expr) {
   const Nvrtc& nv = nvrtc();
   if (!nv.ok) {
     warn_once("libnvrtc.so.12 not found");
     return nullptr;
   }
-  const std::string src = "#define LESB_JIT 1\n#define LESB_JIT_IM " + std::to_string(g.im) + "\n#define LESB_JIT_JM " +
-                          std::to_string(g.jm) + "\n#define LESB_JIT_KM " + std::to_string(g.km) +
-                          "\n#include \"stages_dev.cuh\"\n";
-  const char* headers[] = {JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV};
-  const char* names[] = {"lesb_common.cuh", "stages_dev.cuh"};
+  const char* headers[] = {JIT_SRC_LESB_COMMON, JIT_SRC_STAGES_DEV, JIT_SRC_RESIDENT_DEV};
+  const char* names[] = {"lesb_common.cuh", "stages_dev.cuh", "sor_resident_dev.cuh"};
   nvrtcProgram prog;
-  if (nv.create(&prog, src.c_str(), "lesb_jit.cu", 2, headers, names) != NVRTC_SUCCESS) {
+  if (nv.create(&prog, src.c_str(), "lesb_jit.cu", 3, headers, names) != NVRTC_SUCCESS) {
     warn_once("nvrtcCreateProgram failed");
     return nullptr;
   }
-  const std::string expr = kind == JIT_VELNW_BONDV1 ? (p2 ? "lesb::k_velnw_bondv1<true>" : "lesb::k_velnw_bondv1<false>")
-                                                    : (p2 ? "lesb::k_fused_rhs<true>" : "lesb::k_fused_rhs<false>");
   nv.add_name(prog, expr.c_str());
-  // the ahead-of-time build's floating-point flags (build.py FLAGS)
+  // the ahead-of-time build's floating-point flags (build.py FLAGS); the
+  // CUDA headers for cooperative_groups
+  const char* home = std::getenv("CUDA_HOME");
+  const std::string inc = std::string("--include-path=") + (home ? home : "/usr/local/cuda") + "/include";
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "--prec-div=true",
-                        "--prec-sqrt=true", "--ftz=false", "-lineinfo"};
+                        "--prec-sqrt=true", "--ftz=false", "-lineinfo", inc.c_str()};
   const nvrtcResult rc = nv.compile(prog, sizeof(opts) / sizeof(opts[0]), opts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
@@ -134,6 +140,23 @@ cudaKernel_t compile(int kind, const Geo& g, int p2) {
   return k;
 }
 
+std::mutex g_mu;
+std::map<std::string, cudaKernel_t> g_cache;  // by source + expression
+
+cudaKernel_t cached(const std::string& src, const std::string& expr) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const std::string key = src + "|" + expr;
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return it->second;
+  // (a stream capture in progress must not see the compile's library load)
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaKernel_t k = compile(src, expr);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  g_cache.emplace(key, k);  // (a failure is cached too: the ahead-of-time kernel from then on)
+  return k;
+}
+
 }  // namespace
 
 bool jit_enabled(const Geo& g) {
@@ -145,19 +168,31 @@ bool jit_enabled(const Geo& g) {
 
 cudaKernel_t jit_stage_kernel(int kind, const Geo& g, int p2) {
   if (!jit_enabled(g)) return nullptr;
-  static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int, int>, cudaKernel_t> cache;  // (kind, im, jm, km, p2)
-  std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(kind, g.im, g.jm, g.km, p2 ? 1 : 0);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  // a capture in progress must not see the compile's library load
-  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
-  cudaThreadExchangeStreamCaptureMode(&mode);
-  cudaKernel_t k = compile(kind, g, p2);
-  cudaThreadExchangeStreamCaptureMode(&mode);
-  cache.emplace(key, k);  // (a failure is cached too: the ahead-of-time kernel from then on)
-  return k;
+  const std::string expr = kind == JIT_VELNW_BONDV1 ? (p2 ? "lesb::k_velnw_bondv1<true>" : "lesb::k_velnw_bondv1<false>")
+                                                    : (p2 ? "lesb::k_fused_rhs<true>" : "lesb::k_fused_rhs<false>");
+  return cached(geo_defines(g) + "#include \"stages_dev.cuh\"\n", expr);
+}
+
+cudaKernel_t jit_resident_kernel(const Geo& g, const ResPlan& pl, bool press, bool slab) {
+  static const bool off = std::getenv("LESB_JIT_RES") && std::atoi(std::getenv("LESB_JIT_RES")) == 0;
+  if (off || !jit_enabled(g)) return nullptr;
+  std::string d = geo_defines(g);
+  auto def = [&](const char* n, long long v) { d += std::string("#define LESB_JIT_RES_") + n + " " + std::to_string(v) + "\n"; };
+  def("NI", pl.ni);
+  def("NJ", pl.nj);
+  def("TIM", pl.ti_max);
+  def("TJM", pl.tj_max);
+  def("KK", pl.kk);
+  def("KT", pl.kt);
+  def("FSTRIDE", pl.fstride);
+  def("BSTRIDE", pl.bstride);
+  def("PAD00", pl.pad[0][0]);
+  def("PAD01", pl.pad[0][1]);
+  def("PAD10", pl.pad[1][0]);
+  def("PAD11", pl.pad[1][1]);
+  const std::string expr = std::string("lesb::k_sor_resident<") + (press ? "true" : "false") + ", " +
+                           (slab ? "true" : "false") + ">";
+  return cached(d + "#include \"sor_resident_dev.cuh\"\n", expr);
 }
 
 }  // namespace lesb

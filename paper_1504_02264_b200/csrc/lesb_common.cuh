@@ -92,4 +92,39 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
   return r;  // valid in thread 0
 }
 
+// device-side step bookkeeping for asynchronous runs (capi.cu)
+struct StepBook {
+  unsigned flags;       // stage bits of the current (or first failing) step
+  unsigned steps;       // steps enqueued and completed on the device
+  int fail_step;        // -1 while no step failed
+  unsigned fail_flags;  // stage bits of the first failing step
+  unsigned err;         // device-side solver error (neighbour wait timed out)
+};
+
+// the end-of-step update (one thread, after every stage's flags are final)
+__device__ __forceinline__ void step_book_update(StepBook* b) {
+  if (b->flags && b->fail_step < 0) {
+    b->fail_step = (int)b->steps;
+    b->fail_flags = b->flags;
+  }
+  b->steps += 1;
+}
+
+
+// The geometry a step kernel works with: its launch parameter, or in a
+// runtime-specialised build the same values as constants, so every neighbour
+// offset folds into the load instructions (the ahead-of-time kernels spend a
+// tenth of their instructions on 64-bit address arithmetic).
+__device__ __forceinline__ Geo jit_geo(const Geo& g_in) {
+  Geo g = g_in;
+#ifdef LESB_JIT_IM
+  g.im = LESB_JIT_IM;
+  g.jm = LESB_JIT_JM;
+  g.km = LESB_JIT_KM;
+  g.sj = LESB_JIT_KM + 2;
+  g.si = (long long)(LESB_JIT_JM + 2) * (LESB_JIT_KM + 2);
+#endif
+  return g;
+}
+
 }  // namespace lesb

@@ -33,24 +33,6 @@ struct SorMarks {
 
 // Buffers of the shared-memory-resident red-black solver (sor_resident.cu);
 // use == 0 forces the streaming kernels.
-// device-side step bookkeeping for asynchronous runs (capi.cu)
-struct StepBook {
-  unsigned flags;       // stage bits of the current (or first failing) step
-  unsigned steps;       // steps enqueued and completed on the device
-  int fail_step;        // -1 while no step failed
-  unsigned fail_flags;  // stage bits of the first failing step
-  unsigned err;         // device-side solver error (neighbour wait timed out)
-};
-
-// the end-of-step update (one thread, after every stage's flags are final)
-__device__ __forceinline__ void step_book_update(StepBook* b) {
-  if (b->flags && b->fail_step < 0) {
-    b->fail_step = (int)b->steps;
-    b->fail_flags = b->flags;
-  }
-  b->steps += 1;
-}
-
 // Streaming passes on x-slabs: the plane exchange fused into the pass
 // kernel (sor_split.cu).  Each slab keeps two ghost planes (from the west,
 // from the east) of 4 slots x SplitGeo::spi (value, tag) 64-bit words; the
@@ -117,6 +99,9 @@ void launch_check_finite(const float* a, long long n, unsigned* flags, unsigned 
 enum { JIT_VELNW_BONDV1 = 0, JIT_FUSED_RHS = 1 };
 bool jit_enabled(const Geo& g);
 cudaKernel_t jit_stage_kernel(int kind, const Geo& g, int p2);
+struct ResPlan;
+// the resident solver with this geometry and tile plan as constants, or nullptr
+cudaKernel_t jit_resident_kernel(const Geo& g, const ResPlan& pl, bool press, bool slab);
 
 // sor.cu
 int sor_blocks_rb(const Geo& g);

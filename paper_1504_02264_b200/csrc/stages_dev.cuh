@@ -9,21 +9,6 @@
 
 namespace lesb {
 
-// The geometry a step kernel works with: its launch parameter, or in a
-// runtime-specialised build the same values as constants, so every neighbour
-// offset folds into the load instructions (the ahead-of-time kernels spend a
-// tenth of their instructions on 64-bit address arithmetic).
-__device__ __forceinline__ Geo jit_geo(const Geo& g_in) {
-  Geo g = g_in;
-#ifdef LESB_JIT_IM
-  g.im = LESB_JIT_IM;
-  g.jm = LESB_JIT_JM;
-  g.km = LESB_JIT_KM;
-  g.sj = LESB_JIT_KM + 2;
-  g.si = (long long)(LESB_JIT_JM + 2) * (LESB_JIT_KM + 2);
-#endif
-  return g;
-}
 
 // ---------------------------------------------------------------------------
 // velnw point updates (les.py:226-241):  f + dt*(fgh_a - ((p[+a]-p)*2)/(s[n]+s[n+1]))
