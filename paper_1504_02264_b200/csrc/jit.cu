@@ -170,7 +170,12 @@ cudaKernel_t jit_stage_kernel(int kind, const Geo& g, int p2) {
   if (!jit_enabled(g)) return nullptr;
   const std::string expr = kind == JIT_VELNW_BONDV1 ? (p2 ? "lesb::k_velnw_bondv1<true>" : "lesb::k_velnw_bondv1<false>")
                                                     : (p2 ? "lesb::k_fused_rhs<true>" : "lesb::k_fused_rhs<false>");
-  return cached(geo_defines(g) + "#include \"stages_dev.cuh\"\n", expr);
+  // the fused kernel's blocks-per-SM bound: 10 (51 registers) with the geometry as
+  // constants -- 57.3 against 58.6 us at 8 (64 registers), the ahead-of-time
+  // build's best (LESB_JIT_FUSED_MINB overrides)
+  static const char* minb_env = std::getenv("LESB_JIT_FUSED_MINB");
+  const std::string extra = std::string("#define FUSED_MINB ") + (minb_env ? minb_env : "10") + "\n";
+  return cached(geo_defines(g) + extra + "#include \"stages_dev.cuh\"\n", expr);
 }
 
 cudaKernel_t jit_resident_kernel(const Geo& g, const ResPlan& pl, bool press, bool slab) {

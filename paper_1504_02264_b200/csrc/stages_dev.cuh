@@ -404,10 +404,14 @@ __global__ void k_divergence(Geo g, Spac s, const float* __restrict__ u, const f
 // Reads the post-bondv1 velocities B; writes masked velocities to A, fgh,
 // fgh_old (interior: full chain; halo: adam only), and rhs (interior).
 // ---------------------------------------------------------------------------
+// (128, 8): 64 registers; measured fastest ahead of time (62.6 us at
+// 150^2x90 against 68-72 us at 48-94 registers); the specialised build
+// (jit.cu) uses 10
+#ifndef FUSED_MINB
+#define FUSED_MINB 8
+#endif
 template <bool P2>
-// (128, 8): 64 registers; measured fastest (62.6 us at 150^2x90 against
-// 68-72 us at 48-94 registers)
-__global__ void __launch_bounds__(128, 8) k_fused_rhs(Geo g_in, Spac s, const float* __restrict__ ub, const float* __restrict__ vb,
+__global__ void __launch_bounds__(128, FUSED_MINB) k_fused_rhs(Geo g_in, Spac s, const float* __restrict__ ub, const float* __restrict__ vb,
                             const float* __restrict__ wb, const float* __restrict__ mask,
                             float* __restrict__ fgh, float* __restrict__ fgh_old, float* __restrict__ ua,
                             float* __restrict__ va, float* __restrict__ wa, float* __restrict__ rhs, float vn,
