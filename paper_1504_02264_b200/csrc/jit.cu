@@ -81,8 +81,23 @@ void warn_once(const std::string& what) {
 }
 
 std::string geo_defines(const Geo& g) {
-  return "#define LESB_JIT 1\n#define LESB_JIT_IM " + std::to_string(g.im) + "\n#define LESB_JIT_JM " +
-         std::to_string(g.jm) + "\n#define LESB_JIT_KM " + std::to_string(g.km) + "\n";
+  std::string d = "#define LESB_JIT 1\n#define LESB_JIT_IM " + std::to_string(g.im) + "\n#define LESB_JIT_JM " +
+                  std::to_string(g.jm) + "\n#define LESB_JIT_KM " + std::to_string(g.km) + "\n";
+  // LESB_JIT_DEFINES="NAME=VALUE;...": extra macros for the specialised builds
+  // (device-side build switches, for experiments)
+  if (const char* extra = std::getenv("LESB_JIT_DEFINES")) {
+    std::string e(extra);
+    size_t pos = 0;
+    while (pos < e.size()) {
+      size_t end = e.find(';', pos);
+      if (end == std::string::npos) end = e.size();
+      std::string item = e.substr(pos, end - pos);
+      const size_t eq = item.find('=');
+      if (!item.empty()) d += "#define " + (eq == std::string::npos ? item : item.substr(0, eq) + " " + item.substr(eq + 1)) + "\n";
+      pos = end + 1;
+    }
+  }
+  return d;
 }
 
 // one kernel of `src` (which includes the embedded headers), by its name
