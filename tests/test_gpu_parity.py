@@ -325,3 +325,42 @@ def test_solver_path_selection(P):
     assert path in (1, 2, 3)
     lib = N.load()
     assert lib.lesb_sor_path_in_use(h.h, 1) == 1  # twinned always streams
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_config2_anchors_ahead_of_time_kernels(path):
+    """The config-2 anchors with runtime specialisation off (LESB_JIT=0, in a
+    fresh process: the switch is read once): the ahead-of-time kernels the
+    library falls back to are checked at full size too (the in-process tests
+    above run the specialised ones at 150^2)."""
+    rec = META.get("config2")
+    if rec is None:
+        pytest.skip("large golden vectors not generated")
+    import json as _json
+    import subprocess
+    import sys as _sys
+
+    code = f"""
+import hashlib, json, sys
+sys.path.insert(0, {os.path.dirname(__file__)!r})
+import golden_inputs as gi
+import paper_1504_02264_b200 as P
+P.runtime.set_sor_path({path})
+st = gi.config2_state()
+g = P.Grid(st["im"], st["jm"], st["km"], st["dx1"], st["dy1"], st["dzn"])
+fs = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask"):
+    getattr(fs, n)[...] = st[n]
+inflow = P.WindProfile(*gi.default_inflow(90))
+P.les.step(fs, inflow)
+import numpy as np
+print(json.dumps({{n: hashlib.sha256(np.ascontiguousarray(getattr(fs, n)).tobytes()).hexdigest()[:16]
+                  for n in ("u", "v", "w", "fgh", "fgh_old", "p")}}))
+"""
+    env = dict(os.environ, LESB_JIT="0")
+    r = subprocess.run([_sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = _json.loads(r.stdout.strip().splitlines()[-1])
+    for n, h in got.items():
+        assert h == rec["step1"][n], n
