@@ -121,7 +121,8 @@ cudaKernel_t compile(const std::string& src, const std::string& expr) {
   const char* home = std::getenv("CUDA_HOME");
   const std::string inc = std::string("--include-path=") + (home ? home : "/usr/local/cuda") + "/include";
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "--prec-div=true",
-                        "--prec-sqrt=true", "--ftz=false", "-lineinfo", inc.c_str()};
+                        "--prec-sqrt=true", "--ftz=false", "-lineinfo", inc.c_str(),
+                        "--include-path=/usr/local/cuda/include"};
   const nvrtcResult rc = nv.compile(prog, sizeof(opts) / sizeof(opts[0]), opts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
