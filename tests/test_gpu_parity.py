@@ -364,3 +364,43 @@ print(json.dumps({{n: hashlib.sha256(np.ascontiguousarray(getattr(fs, n)).tobyte
     got = _json.loads(r.stdout.strip().splitlines()[-1])
     for n, h in got.items():
         assert h == rec["step1"][n], n
+
+
+@pytest.mark.parametrize("dims", [(170, 110, 70), (120, 130, 91)])
+def test_specialised_equals_ahead_of_time(dims):
+    """Other large geometries (other tile plans, odd km): three steps with the
+    runtime-specialised kernels in one process and with LESB_JIT=0 in another,
+    on the resident and the colour-split paths -- every field bitwise equal."""
+    import subprocess
+    import sys as _sys
+
+    code = f"""
+import hashlib, json, sys
+sys.path.insert(0, {os.path.dirname(__file__)!r})
+import numpy as np
+import golden_inputs as gi
+import paper_1504_02264_b200 as P
+out = {{}}
+for path in (0, 1):
+    P.runtime.set_sor_path(path)
+    st = gi.random_state(*{dims!r}, seed=11, uniform=True, vel_scale=0.3)
+    g = P.Grid(st["im"], st["jm"], st["km"], st["dx1"], st["dy1"], st["dzn"])
+    fs = P.FlowState.create(g, dt=st["dt"], vn=st["vn"], cs=st["cs"])
+    for n in ("u", "v", "w", "fgh", "fgh_old", "p", "mask"):
+        getattr(fs, n)[...] = st[n]
+    inflow = P.WindProfile(*gi.random_inflow({dims[2]}, seed=3))
+    for _ in range(3):
+        P.les.step(fs, inflow)
+    out[path] = {{n: hashlib.sha256(np.ascontiguousarray(getattr(fs, n)).tobytes()).hexdigest()[:16]
+                 for n in ("u", "v", "w", "fgh", "fgh_old", "p")}}
+print(json.dumps(out))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for jit in ("1", "0"):
+        r = subprocess.run([_sys.executable, "-c", code], env=dict(os.environ, LESB_JIT=jit), capture_output=True,
+                           text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert "runtime specialisation off" not in r.stderr or jit == "0", r.stderr[-500:]
+        res[jit] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["1"] == res["0"]
