@@ -101,6 +101,20 @@ int lesb_set_coeffs(lesb_handle h, const lesb_coeffs* c);          /* FlowState.
 int lesb_set_physics(lesb_handle h, float dt, float vn, float cs, const float* csd2, float csd2_scalar);
 int lesb_upload(lesb_handle h, int field, const float* host);       /* host -> device, full halo array */
 int lesb_download(lesb_handle h, int field, float* host);           /* device -> host */
+/* Asynchronous state copies, overlapping the steps (no reference counterpart:
+ * the reference's FlowState arrays are host numpy, les.py:37-71; these serve
+ * its dump / restart pattern, dump.py:42-56 and cli.py:202-219, without
+ * stalling the device).  lesb_stage_upload starts the host -> device copy of
+ * `host` (pinned for overlap) into the field's staging buffer and returns;
+ * `host` must stay unchanged until the next synchronising call after
+ * lesb_stage_commit, which enqueues the staged fields becoming the state at
+ * that point of the domain's stream.  lesb_download_async enqueues a snapshot
+ * of the field as of that point and its copy to `host`; lesb_copies_wait
+ * blocks until every staged and asynchronous copy has finished. */
+int lesb_stage_upload(lesb_handle h, int field, const float* host);
+int lesb_stage_commit(lesb_handle h);
+int lesb_download_async(lesb_handle h, int field, float* host);
+int lesb_copies_wait(lesb_handle h);
 void* lesb_device_ptr(lesb_handle h, int field);                    /* plumbing for NCCL halo exchange */
 void* lesb_stream(lesb_handle h);                                   /* the domain's cudaStream_t */
 int lesb_synchronize(lesb_handle h);

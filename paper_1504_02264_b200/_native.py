@@ -54,6 +54,10 @@ _SIGS = {
     "lesb_set_physics": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, FP, C.c_float]),
     "lesb_upload": (C.c_int, [C.c_void_p, C.c_int, FP]),
     "lesb_download": (C.c_int, [C.c_void_p, C.c_int, FP]),
+    "lesb_stage_upload": (C.c_int, [C.c_void_p, C.c_int, FP]),
+    "lesb_stage_commit": (C.c_int, [C.c_void_p]),
+    "lesb_download_async": (C.c_int, [C.c_void_p, C.c_int, FP]),
+    "lesb_copies_wait": (C.c_int, [C.c_void_p]),
     "lesb_device_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
     "lesb_stream": (C.c_void_p, [C.c_void_p]),
     "lesb_synchronize": (C.c_int, [C.c_void_p]),

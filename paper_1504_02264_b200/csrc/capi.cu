@@ -78,6 +78,45 @@ __global__ void k_step_tail(StepBook* b) {
   if (threadIdx.x == 0 && blockIdx.x == 0) step_book_update(b);
 }
 
+// The synchronous step moves its inflow in and its residuals and flags out
+// through host-mapped pinned memory with these kernels instead of copy-engine
+// memcpys: the bulk copies of lesb_stage_upload / lesb_download_async run on
+// the copy engines meanwhile, and a step's small copies would queue behind
+// them (one direction's copies are served in order).
+__global__ void k_step_head(float* __restrict__ in_d, const float* __restrict__ in_h, int n, StepBook* b) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) in_d[i] = in_h[i];
+  if (threadIdx.x == 0) {
+    b->flags = 0;
+    b->err = 0;
+  }
+}
+
+__global__ void k_step_out(double* __restrict__ res_h, const double* __restrict__ res_d, int n,
+                           StepBook* __restrict__ book_h, const StepBook* __restrict__ book_d) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) res_h[i] = res_d[i];
+  if (threadIdx.x == 0) *book_h = *book_d;
+}
+
+__global__ void k_word_out(unsigned* dst_h, const unsigned* src_d) { *dst_h = *src_d; }
+
+// device-to-device field copy (staged commit, snapshot): a kernel, for the
+// same reason
+__global__ void k_copy_field(float* __restrict__ dst, const float* __restrict__ src, long long n) {
+  const long long n4 = n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) d4[i] = s4[i];
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) dst[4 * n4 + threadIdx.x] = src[4 * n4 + threadIdx.x];
+}
+
+cudaError_t copy_field(float* dst, const float* src, long long n, int device, cudaStream_t st) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  k_copy_field<<<4 * sms, 512, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
 int first_stage(unsigned bits) {
   for (int s = 0; s < 7; ++s)
     if (bits & (1u << s)) return s;
@@ -147,6 +186,15 @@ struct lesb_domain {
   void* gxbuf = nullptr;
   unsigned* gepoch = nullptr;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // asynchronous state copies (lesb_stage_upload / lesb_download_async): an
+  // upload and a download stream beside `st`, a device staging buffer and a
+  // device snapshot buffer per field, events ordering their reuse
+  cudaStream_t up_st = nullptr, dn_st = nullptr;
+  float* staged[8] = {};
+  float* snap[8] = {};
+  unsigned staged_mask = 0;
+  cudaEvent_t ev_up = nullptr, ev_commit = nullptr, ev_snap = nullptr;
+  cudaEvent_t ev_dn[8] = {};  // per field: the last download from its snapshot buffer
   bool known_finite = false;
   long long n_alloc = 0;  // (im+3)*si
   long long n_py = 0;     // (im+2)*si : the Python-visible array
@@ -524,17 +572,12 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
   if (rc) return rc;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  if (mode == MODE_SYNC) {
-    cudaMemsetAsync(&h->book_d->flags, 0, sizeof(unsigned), h->st);
-    cudaMemsetAsync(&h->book_d->err, 0, sizeof(unsigned), h->st);
-    cudaMemcpyAsync(h->inflow_d, h->inflow_h, 3 * h->g.km * sizeof(float), cudaMemcpyHostToDevice, h->st);
-  }
+  if (mode == MODE_SYNC) k_step_head<<<1, 256, 0, h->st>>>(h->inflow_d, h->inflow_h, 3 * h->g.km, h->book_d);
   bool tail_done = false;
   cudaError_t body_err =
       enqueue_step_body(h, n_iter, scheme, omega, mode == MODE_ASYNC ? h->book_d : nullptr, &tail_done);
   if (mode == MODE_SYNC) {
-    cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st);
-    cudaMemcpyAsync(h->book_h, h->book_d, sizeof(StepBook), cudaMemcpyDeviceToHost, h->st);
+    k_step_out<<<1, 256, 0, h->st>>>(h->res_h, h->res_d, n_iter, h->book_h, h->book_d);
   } else if (!tail_done) {
     k_step_tail<<<1, 32, 0, h->st>>>(h->book_d);
   }
@@ -564,7 +607,8 @@ int scan_finite(lesb_domain* h, bool* ok) {
   launch_check_finite(h->p, h->n_py, fl, 1, h->st);
   launch_check_finite(h->fgh, 3 * h->n_py, fl, 1, h->st);
   launch_check_finite(h->fgh_old, 3 * h->n_py, fl, 1, h->st);
-  CK(cudaMemcpyAsync(&h->book_h->flags, fl, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  k_word_out<<<1, 1, 0, h->st>>>(&h->book_h->flags, fl);
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->st));
   *ok = h->book_h->flags == 0;
   return LESB_OK;
@@ -716,6 +760,18 @@ int lesb_destroy(lesb_handle h) {
   if (h->inflow_h) cudaFreeHost(h->inflow_h);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  if (h->up_st) cudaStreamSynchronize(h->up_st);
+  if (h->dn_st) cudaStreamSynchronize(h->dn_st);
+  for (int f = 0; f < 8; ++f) {
+    if (h->staged[f]) cudaFree(h->staged[f]);
+    if (h->snap[f]) cudaFree(h->snap[f]);
+  }
+  for (cudaEvent_t e : {h->ev_up, h->ev_commit, h->ev_snap})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_dn)
+    if (e) cudaEventDestroy(e);
+  if (h->up_st) cudaStreamDestroy(h->up_st);
+  if (h->dn_st) cudaStreamDestroy(h->dn_st);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
   return LESB_OK;
@@ -796,6 +852,86 @@ int lesb_download(lesb_handle h, int field, float* host) {
   CK(cudaSetDevice(h->device));
   CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(host, d, field_count(h, field) * sizeof(float), cudaMemcpyDeviceToHost));
+  return LESB_OK;
+}
+
+// ---- asynchronous state copies ----
+// The copies run on their own streams so they overlap the steps enqueued on
+// `st`: a staged upload lands in a device staging buffer and becomes the
+// state at lesb_stage_commit (a device-to-device copy ordered on `st`); an
+// asynchronous download snapshots the field on `st` (device-to-device, so
+// later steps may overwrite the field at once) and copies the snapshot to
+// the host on the download stream.  Buffers are reused only after the copy
+// that last read them (ev_commit / the field's ev_dn: one event for all
+// fields would hold the domain stream until the previous field's download
+// had finished).
+static int ensure_copy_streams(lesb_domain* h) {
+  if (h->up_st) return LESB_OK;
+  CK(cudaStreamCreateWithFlags(&h->up_st, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->dn_st, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&h->ev_up, &h->ev_commit, &h->ev_snap})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t& e : h->ev_dn) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return LESB_OK;
+}
+
+int lesb_stage_upload(lesb_handle h, int field, const float* host) {
+  if (!h || !host) return fail(LESB_E_ARG, "null argument");
+  if (!field_ptr(h, field)) return fail(LESB_E_ARG, "unknown field id");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  int rc = ensure_copy_streams(h);
+  if (rc) return rc;
+  const size_t bytes = field_count(h, field) * sizeof(float);
+  if (!h->staged[field]) CK(cudaMalloc(&h->staged[field], bytes));
+  CK(cudaStreamWaitEvent(h->up_st, h->ev_commit, 0));  // the last commit has read the staging buffer
+  CK(cudaMemcpyAsync(h->staged[field], host, bytes, cudaMemcpyHostToDevice, h->up_st));
+  h->staged_mask |= 1u << field;
+  return LESB_OK;
+}
+
+int lesb_stage_commit(lesb_handle h) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  if (!h->staged_mask) return LESB_OK;
+  CK(cudaEventRecord(h->ev_up, h->up_st));
+  CK(cudaStreamWaitEvent(h->st, h->ev_up, 0));
+  for (int f = 0; f < 8; ++f) {
+    if (!(h->staged_mask & (1u << f))) continue;
+    CK(copy_field(field_ptr(h, f), h->staged[f], field_count(h, f), h->device, h->st));
+    if (f != LESB_MASK && f != LESB_RHS) h->known_finite = false;
+  }
+  CK(cudaEventRecord(h->ev_commit, h->st));
+  h->staged_mask = 0;
+  return LESB_OK;
+}
+
+int lesb_download_async(lesb_handle h, int field, float* host) {
+  if (!h || !host) return fail(LESB_E_ARG, "null argument");
+  float* d = field_ptr(h, field);
+  if (!d) return fail(LESB_E_ARG, "unknown field id");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  int rc = ensure_copy_streams(h);
+  if (rc) return rc;
+  const size_t bytes = field_count(h, field) * sizeof(float);
+  if (!h->snap[field]) CK(cudaMalloc(&h->snap[field], bytes));
+  CK(cudaStreamWaitEvent(h->st, h->ev_dn[field], 0));  // the last download has read this snapshot buffer
+  CK(copy_field(h->snap[field], d, field_count(h, field), h->device, h->st));
+  CK(cudaEventRecord(h->ev_snap, h->st));
+  CK(cudaStreamWaitEvent(h->dn_st, h->ev_snap, 0));
+  CK(cudaMemcpyAsync(host, h->snap[field], bytes, cudaMemcpyDeviceToHost, h->dn_st));
+  CK(cudaEventRecord(h->ev_dn[field], h->dn_st));
+  return LESB_OK;
+}
+
+int lesb_copies_wait(lesb_handle h) {
+  if (!h) return fail(LESB_E_ARG, "null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CK(cudaSetDevice(h->device));
+  if (h->up_st) CK(cudaStreamSynchronize(h->up_st));
+  if (h->dn_st) CK(cudaStreamSynchronize(h->dn_st));
   return LESB_OK;
 }
 

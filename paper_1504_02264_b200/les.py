@@ -28,7 +28,7 @@ from .reftypes import Grid, NumericsError, Scheme, SorCoeffs, is_redblack, is_tw
 from .sor import PressureHalo, build_uniform_coeffs
 
 __all__ = [
-    "FlowState", "step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf",
+    "FlowState", "PendingCopies", "step", "velnw", "bondv1", "velfg_merged", "velfg_twopass", "feedbf",
     "strain_magnitude", "les_viscosity", "adam", "divergence", "press", "_pressure_halo",
     "STAGES", "run_steps", "les_main", "refresh_pressure_faces", "run_boundary_audit",
 ]
@@ -86,6 +86,7 @@ class FlowState:
         self.__dict__["_h"] = None
         self.__dict__["_pushed_phys"] = None
         self.__dict__["_pushed_coeffs"] = None
+        self.__dict__["_staged"] = {}
         for n, a in zip(_ALL, (u, v, w, fgh, fgh_old, p, mask)):
             self._host[n] = a
         self.grid = grid
@@ -134,6 +135,57 @@ class FlowState:
             self._pull(n)
         return self
 
+    # -- asynchronous copies (overlap with the steps) --------------------------
+    def stage(self, **arrays) -> "FlowState":
+        """Start copying ``arrays`` (field name -> array of that field's
+        shape) to the device without changing the state; they become the state
+        at ``commit_staged()``.  The copies overlap device work (fully when the
+        arrays are pinned); the arrays must stay unchanged until the first
+        device operation after the commit has returned."""
+        h = self.handle()
+        for n, a in arrays.items():
+            if n not in _FIELD_ID:
+                raise ValueError(f"unknown field {n!r}")
+            a = N.f32c(np.asarray(a))
+            if a.shape != self._shape(n):
+                raise ValueError(f"field {n} has shape {a.shape}, expected {self._shape(n)}")
+            h.call("lesb_stage_upload", _FIELD_ID[n], N.fptr(a))
+            self._staged[n] = a
+        return self
+
+    def commit_staged(self) -> "FlowState":
+        """The staged arrays become the state, in order with the device work
+        (as if assigned: ``state.u = a``; a later read of ``state.u`` refreshes
+        ``a`` in place)."""
+        if not self._staged:
+            return self
+        self._lent.difference_update(self._staged)
+        h = self.handle()
+        h.call("lesb_stage_commit")
+        for n, a in self._staged.items():
+            self._host[n] = a
+            self._dev_newer.discard(n)
+        self._staged.clear()
+        return self
+
+    def download_async(self, out: dict) -> "PendingCopies":
+        """Enqueue copies of the fields named by ``out`` (name -> float32
+        C-contiguous array of the field's shape; pinned memory overlaps fully)
+        as they stand after the device work enqueued so far, and return at
+        once.  Later steps do not disturb the copies (the device snapshots
+        the fields first).  The arrays are complete after ``wait()`` on the
+        returned object."""
+        h = self.handle()
+        for n, a in out.items():
+            if n not in _FIELD_ID:
+                raise ValueError(f"unknown field {n!r}")
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+                    and a.flags.writeable and a.shape == self._shape(n)):
+                raise ValueError(f"out[{n!r}] must be a writeable C-contiguous float32 array of shape "
+                                 f"{self._shape(n)}")
+            h.call("lesb_download_async", _FIELD_ID[n], N.fptr(a))
+        return PendingCopies(h, out)
+
     def handle(self) -> _Handle:
         """The device domain, with host-side changes uploaded."""
         if self._h is None:
@@ -170,6 +222,18 @@ class FlowState:
     def __repr__(self):
         g = self.grid
         return f"FlowState(device, {g.im}x{g.jm}x{g.km}, dt={self.dt}, vn={self.vn}, cs={self.cs})"
+
+
+class PendingCopies:
+    """Asynchronous downloads in flight (FlowState.download_async)."""
+
+    def __init__(self, h: _Handle, out: dict):
+        self._h = h
+        self.out = out
+
+    def wait(self) -> dict:
+        self._h.call("lesb_copies_wait")
+        return self.out
 
 
 def _field_property(name):
