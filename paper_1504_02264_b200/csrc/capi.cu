@@ -572,7 +572,10 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
   if (rc) return rc;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  if (mode == MODE_SYNC) k_step_head<<<1, 256, 0, h->st>>>(h->inflow_d, h->inflow_h, 3 * h->g.km, h->book_d);
+  if (mode == MODE_SYNC) {  // (every inflow word read in one round: host reads are slow under bulk copies)
+    const int n_in = 3 * h->g.km, nt = std::min(1024, (n_in + 31) / 32 * 32);
+    k_step_head<<<1, nt, 0, h->st>>>(h->inflow_d, h->inflow_h, n_in, h->book_d);
+  }
   bool tail_done = false;
   cudaError_t body_err =
       enqueue_step_body(h, n_iter, scheme, omega, mode == MODE_ASYNC ? h->book_d : nullptr, &tail_done);
