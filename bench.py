@@ -307,7 +307,8 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    multi = world > 1 or args.slabs  # x-slab path (--slabs: on one rank, under torch.distributed.run)
+    if multi:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
 
@@ -320,7 +321,7 @@ def run_gpu(args):
     st0 = gi.config2_state(IM, JM, KM)
     inflow = P.WindProfile(*gi.default_inflow(KM))
     slab_dom = None
-    if world == 1:
+    if not multi:
         grid = P.Grid(IM, JM, KM, st0["dx1"], st0["dy1"], st0["dzn"])
 
         def make_state():
@@ -387,7 +388,7 @@ def run_gpu(args):
     sor_path = {1: "streaming colour passes, colour-split layout", 2: "shared-memory-resident persistent kernel",
                 3: "streaming colour passes, natural layout"}[
         lib.lesb_sor_path_in_use(hw.h, 0)]
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     t_wall = time.perf_counter()
@@ -422,7 +423,7 @@ def run_gpu(args):
             phase_ms += ph
     torch.cuda.synchronize()
     N.check(lib.lesb_set_timing(hw.h, 0), "set_timing")
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     done = N.C.c_int(0)
@@ -433,7 +434,7 @@ def run_gpu(args):
         raise RuntimeError(f"benchmark state went non-finite at step {fstep.value} ({fstage.value})")
     step_ms = [a.elapsed_time(b) for a, b in ev]
     dev_ms = float(sum(step_ms))
-    if world > 1:
+    if multi:
         t = torch.tensor([dev_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
@@ -464,11 +465,15 @@ def run_gpu(args):
         e2e = e2e_run(P, N, gi, torch, grid, st0, inflow, args)
     else:
         e2e = e2e_slabs(slab_dom, gstate, inflow, torch, args, world)
-    if world > 1 and e2e["value"] is not None:
+    if multi and e2e["value"] is not None:
         t = torch.tensor([e2e["seconds"]], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e["value"] *= e2e["seconds"] / float(t.item())
         e2e["seconds"] = float(t.item())
+        if "serial_seconds" in e2e:
+            t = torch.tensor([e2e["serial_seconds"]], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["serial_value"] *= e2e["serial_seconds"] / float(t.item())
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -485,7 +490,7 @@ def run_gpu(args):
             "method": {"reinit_every_steps": REINIT,
                        "timing": "CUDA events on the domain stream around each CUDA-graph step replay",
                        "sor_kernel": sor_path,
-                       "exchange": "NCCL halo planes inside the step graph" if world > 1 else None},
+                       "exchange": "NCCL halo planes inside the step graph" if multi else None},
             "mlups": value * n_int / 1e6,
             "step_roofline": {"bytes_per_cell": B_STEP, "achieved_gbs": step_gbs, "peak_gbs": hbm,
                               "frac": step_gbs / hbm, "peak_kind": peak_kind},
@@ -509,10 +514,10 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "wall_s": wall,
         }
-        if world == 1 and not args.grid and not args.no_extras:
+        if not multi and not args.grid and not args.no_extras:
             line["extras"] = side_lines()
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 
@@ -623,29 +628,62 @@ def e2e_run(P, N, gi, torch, grid, st0, inflow, args):
 
 
 def e2e_slabs(dom, gstate, inflow, torch, args, world):
-    """Public slab API with host buffers (upload, steps, download) per window."""
+    """Public slab API with host buffers, e2e_run's windows on every rank:
+    the rank's part of the initial state staged from pinned host memory
+    during the previous window (SlabDomain.stage / commit_staged), its slab
+    fields downloaded to pinned host memory during the next
+    (SlabDomain.download_async); `serial_value`: upload / steps / download in
+    sequence."""
     names = ("u", "v", "w", "fgh", "fgh_old", "p", "mask")
+    ins = {}
+    for n in names:
+        ins[n] = torch.empty(gstate[n].shape, dtype=torch.float32, pin_memory=True).numpy()
+        ins[n][...] = gstate[n]
+    outs = [{n: torch.empty(dom.slab_shape(n), dtype=torch.float32, pin_memory=True).numpy() for n in names[:6]}
+            for _ in range(2)]
 
-    def window():
+    def pipelined(n_windows):
+        pend = [None, None]
+        dom.stage(ins)
+        for w in range(n_windows):
+            dom.commit_staged()
+            dom.step(inflow)
+            if w + 1 < n_windows:
+                dom.stage(ins)
+            for _s in range(REINIT - 1):
+                dom.step(inflow)
+            b = w % 2
+            if pend[b] is not None:
+                pend[b].wait()
+            pend[b] = dom.download_async(outs[b])
+        for p in pend:
+            if p is not None:
+                p.wait()
+
+    def serial():
         dom.upload(gstate)
         for _s in range(REINIT):
             dom.step(inflow)
         for n in names[:6]:
             dom.slab.download(n, JM, KM)
 
-    window()
-    n_windows = max(1, args.steps // REINIT)
-    secs = 0.0
-    for _ in range(n_windows):
+    def timed(fn, *a):
         torch.cuda.synchronize()
         dom.dist.barrier()
         t0 = time.perf_counter()
-        window()
-        secs += time.perf_counter() - t0
-    per_slab = sum(gstate[n].nbytes for n in names) / world
-    h2d = per_slab / REINIT + 3 * KM * 4
-    d2h = per_slab * 6 / 7 / REINIT + 4
-    return {"value": world * n_windows * REINIT / secs, "seconds": secs, "h2d": int(h2d), "d2h": int(d2h)}
+        fn(*a)
+        return time.perf_counter() - t0
+
+    pipelined(1)
+    n_windows = max(E2E_MIN_WINDOWS, -(-args.steps // REINIT))
+    secs = timed(pipelined, n_windows)
+    s_windows = max(1, args.steps // REINIT)
+    s_secs = sum(timed(serial) for _ in range(s_windows))
+    slab_bytes = {n: 4 * int(np.prod(dom.slab_shape(n))) for n in names}  # the rank's part, halo planes included
+    h2d = sum(slab_bytes.values()) / REINIT + 3 * KM * 4
+    d2h = sum(slab_bytes[n] for n in names[:6]) / REINIT + 4
+    return {"value": world * n_windows * REINIT / secs, "seconds": secs, "h2d": int(h2d), "d2h": int(d2h),
+            "windows": n_windows, "serial_value": world * s_windows * REINIT / s_secs, "serial_seconds": s_secs}
 
 
 def main():
@@ -657,6 +695,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e measurement (profiling runs)")
+    ap.add_argument("--slabs", action="store_true",
+                    help="the x-slab (N-GPU) path even on one rank (launch under torch.distributed.run)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the side lines (config 3 press-only at 512^2, the 300^2 step) measured after the run")
     ap.add_argument("--grid", type=int, nargs=3, metavar=("IM", "JM", "KM"),

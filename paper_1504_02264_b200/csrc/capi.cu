@@ -99,6 +99,8 @@ __global__ void k_step_out(double* __restrict__ res_h, const double* __restrict_
 
 __global__ void k_word_out(unsigned* dst_h, const unsigned* src_d) { *dst_h = *src_d; }
 
+__global__ void k_set_word(int* dst, int v) { *dst = v; }
+
 // device-to-device field copy (staged commit, snapshot): a kernel, for the
 // same reason
 __global__ void k_copy_field(float* __restrict__ dst, const float* __restrict__ src, long long n) {
@@ -166,6 +168,7 @@ struct lesb_domain {
   float* split = nullptr;  // colour-split p / rhs of the streaming red-black passes (4 * SplitGeo::n floats)
   void* xbuf = nullptr;       // resident solver face exchange (64-bit words)
   int* coll_d = nullptr;      // NCCL slabs: scratch of the stage reductions
+  int* coll_h = nullptr;      // (pinned, host-mapped: the reduced value)
   // x-slab streaming passes with the fused plane exchange (PassGhost):
   // ghost planes [from west: 4 slots][from east: 4 slots] of spi words, the
   // solve epoch, and (NCCL ranks) the neighbours' ghost buffers mapped
@@ -474,12 +477,18 @@ void nccl_p_hook(void* ctx, float* p, long long plane) {
 // NCCL slabs: reductions over the ranks on the domain stream, synchronous
 // (SURVEY 8(e) C4, C5).  coll_d: 2 ints of scratch.
 int nccl_int_reduce(lesb_domain* h, int* v, ncclRedOp_t op) {
+  // (the value in as a kernel argument and out through host-mapped memory:
+  // no copy-engine work, which would queue behind asynchronous state copies)
   if (!h->coll_d) CK(cudaMalloc(&h->coll_d, 2 * sizeof(int)));
-  CK(cudaMemcpyAsync(h->coll_d, v, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  if (!h->coll_h) CK(cudaMallocHost(&h->coll_h, sizeof(int)));
+  k_set_word<<<1, 1, 0, h->st>>>(h->coll_d, *v);
+  CK(cudaGetLastError());
   if (ncclAllReduce(h->coll_d, h->coll_d + 1, 1, ncclInt, op, h->link.comm, h->st) != ncclSuccess)
     return fail(LESB_E_CUDA, "ncclAllReduce (stage reduction) failed");
-  CK(cudaMemcpyAsync(v, h->coll_d + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  k_word_out<<<1, 1, 0, h->st>>>(reinterpret_cast<unsigned*>(h->coll_h), reinterpret_cast<const unsigned*>(h->coll_d + 1));
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->st));
+  *v = *h->coll_h;
   return LESB_OK;
 }
 
@@ -752,6 +761,7 @@ int lesb_destroy(lesb_handle h) {
   if (h->gepoch) cudaFree(h->gepoch);
   if (h->split) cudaFree(h->split);
   if (h->coll_d) cudaFree(h->coll_d);
+  if (h->coll_h) cudaFreeHost(h->coll_h);
   if (h->gpeer_w) cudaIpcCloseMemHandle(h->gpeer_w);
   if (h->gpeer_e) cudaIpcCloseMemHandle(h->gpeer_e);
   if (h->ghost) cudaFree(h->ghost);
@@ -1112,7 +1122,8 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   if (residuals_out && h->link.comm) {  // C4: the global residual history
     rc = nccl_residuals(h, n_iter);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(h->res_h, h->res_d, n_iter * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    k_step_out<<<1, 256, 0, h->st>>>(h->res_h, h->res_d, n_iter, h->book_h, h->book_d);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->st));
   }
   if (residuals_out) std::memcpy(residuals_out, h->res_h, n_iter * sizeof(double));

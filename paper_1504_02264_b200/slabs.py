@@ -95,6 +95,8 @@ class _Slab:
         h = N.C.c_void_p()
         N.check(lib.lesb_create(N.C.byref(desc), N.C.byref(h)), "lesb_create")
         self.h = h
+        self._staged: list = []
+        self._committed: list = []
         c = build_uniform_coeffs(g)
         keep: list = []
         cf = N.make_coeffs(c, keep)
@@ -110,6 +112,22 @@ class _Slab:
         part = slice_global(np.asarray(global_arr, np.float32), self.i0, self.i1)
         fid = N.LESB_RHS if name == "rhs" else _FIELD_ID[name]
         N.check(self.lib.lesb_upload(self.h, fid, N.fptr(part)), "lesb_upload")
+
+    # asynchronous copies (les.FlowState.stage / commit_staged / download_async)
+    def stage(self, name, global_arr):
+        part = slice_global(np.asarray(global_arr, np.float32), self.i0, self.i1)  # (a view when contiguous)
+        self._staged.append(part)  # alive until the copy has run
+        N.check(self.lib.lesb_stage_upload(self.h, _FIELD_ID[name], N.fptr(part)), "lesb_stage_upload")
+
+    def commit_staged(self):
+        N.check(self.lib.lesb_stage_commit(self.h), "lesb_stage_commit")
+        self._committed, self._staged = self._staged, []  # (dropped at the next commit: the steps between synchronise)
+
+    def download_async(self, name, out):
+        N.check(self.lib.lesb_download_async(self.h, _FIELD_ID[name], N.fptr(out)), "lesb_download_async")
+
+    def copies_wait(self):
+        N.check(self.lib.lesb_copies_wait(self.h), "lesb_copies_wait")
 
     def download(self, name, jm, km):
         shape = (self.im + 2, jm + 2, km + 2) + ((3,) if name in ("fgh", "fgh_old") else ())
@@ -176,6 +194,16 @@ class SlabGroup:
             s.close()
 
 
+class _SlabPending:
+    def __init__(self, slab, out):
+        self._slab = slab
+        self.out = out
+
+    def wait(self) -> dict:
+        self._slab.copies_wait()
+        return self.out
+
+
 class SlabDomain:
     """This rank's x-slab in a one-process-per-GPU run (torch.distributed
     initialised; NCCL for the device exchanges)."""
@@ -200,6 +228,33 @@ class SlabDomain:
     def upload(self, state: dict):
         for name in FIELDS:
             self.slab.upload(name, state[name])
+
+    def stage(self, state: dict):
+        """Start copying this rank's part of the global fields in ``state``
+        (pinned arrays overlap fully) to the device; they become the slab's
+        state at ``commit_staged()`` (les.FlowState.stage)."""
+        for name in FIELDS:
+            if name in state:
+                self.slab.stage(name, state[name])
+
+    def commit_staged(self):
+        self.slab.commit_staged()
+
+    def download_async(self, out: dict):
+        """Enqueue copies of this rank's slab fields into ``out`` (name ->
+        float32 C-contiguous array of the slab's shape, ``slab_shape(name)``)
+        as they stand after the work enqueued so far; ``wait()`` on the
+        returned object completes them (les.FlowState.download_async)."""
+        for n, a in out.items():
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+                    and a.shape == self.slab_shape(n)):
+                raise ValueError(f"out[{n!r}] must be a C-contiguous float32 array of shape {self.slab_shape(n)}")
+            self.slab.download_async(n, a)
+        return _SlabPending(self.slab, out)
+
+    def slab_shape(self, name):
+        g = self.grid
+        return (self.slab.im + 2, g.jm + 2, g.km + 2) + ((3,) if name in ("fgh", "fgh_old") else ())
 
     def step(self, inflow, n_iter: int = 50, scheme: Scheme = Scheme.REDBLACK, residuals: bool = False):
         """One step (les.py:393-416) on every rank.  The library reduces the

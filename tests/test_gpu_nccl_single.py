@@ -102,3 +102,38 @@ def test_single_rank_slab_blowup_stage(nccl_world):
         assert err.value.stage == "velnw"
     finally:
         dom.close()
+
+
+def test_single_rank_slab_async_copies(nccl_world):
+    """SlabDomain.stage / commit_staged / download_async (bench.py's N-GPU
+    e2e windows) on a one-rank NCCL slab: the staged state steps like the
+    uploaded one, and a snapshot taken after step 1 is the step-1 state
+    however many steps follow before the wait."""
+    import paper_1504_02264_b200 as P
+    from paper_1504_02264_b200.slabs import SlabDomain
+
+    dims = (32, 24, 16)
+    st, g, fs = _state(dims, seed=13)
+    inflow = P.WindProfile(*gi.random_inflow(dims[2], seed=4))
+    dom = SlabDomain(g, dt=st["dt"], vn=st["vn"], cs=st["cs"], device=0)
+    names = ("u", "v", "w", "fgh", "fgh_old", "p")
+    try:
+        dom.upload(gi.zero_state(*dims))
+        dom.stage(st)
+        dom.commit_staged()
+        P.les.step(fs, inflow, n_iter=20)
+        dom.step(inflow, n_iter=20)
+        after1 = {n: getattr(fs, n).copy() for n in names}
+        pend = dom.download_async({n: np.empty(dom.slab_shape(n), np.float32) for n in names})
+        for _ in range(3):
+            P.les.step(fs, inflow, n_iter=20)
+            dom.step(inflow, n_iter=20)
+        for n in names:
+            assert bits(dom.slab.download(n, g.jm, g.km), getattr(fs, n)), n
+        got = pend.wait()
+        for n in names:
+            assert bits(got[n], after1[n]), ("snapshot", n)
+        with pytest.raises(ValueError):
+            dom.download_async({"u": np.empty((3, 3, 3), np.float32)})
+    finally:
+        dom.close()
