@@ -91,6 +91,26 @@ __global__ void k_step_head(float* __restrict__ in_d, const float* __restrict__ 
   }
 }
 
+// the inflow as a kernel argument (launched before the step graph): the step
+// then reads nothing from host memory -- a host read waits behind a bulk
+// device-to-host copy's writes on the link
+constexpr int INFLOW_ARG_MAX = 960;  // (3 km floats, within the 4 KB parameter space)
+struct InflowArg {
+  float v[INFLOW_ARG_MAX];
+};
+__global__ void k_step_head_arg(float* __restrict__ in_d, const __grid_constant__ InflowArg in, int n, StepBook* b) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) in_d[i] = in.v[i];
+  if (threadIdx.x == 0) {
+    b->flags = 0;
+    b->err = 0;
+  }
+}
+
+bool inflow_by_arg(int km) {
+  static const bool off = std::getenv("LESB_INFLOW_ARG") && std::atoi(std::getenv("LESB_INFLOW_ARG")) == 0;
+  return !off && 3 * km <= INFLOW_ARG_MAX;
+}
+
 __global__ void k_step_out(double* __restrict__ res_h, const double* __restrict__ res_d, int n,
                            StepBook* __restrict__ book_h, const StepBook* __restrict__ book_d) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) res_h[i] = res_d[i];
@@ -198,6 +218,20 @@ struct lesb_domain {
   unsigned staged_mask = 0;
   cudaEvent_t ev_up = nullptr, ev_commit = nullptr, ev_snap = nullptr;
   cudaEvent_t ev_dn[8] = {};  // per field: the last download from its snapshot buffer
+  // the copies not yet enqueued: a synchronous step enqueues one chunk of
+  // each direction after its launch (so the link carries at most one chunk
+  // while the step's own transfers run); commit / a reused snapshot buffer /
+  // lesb_copies_wait enqueue the rest at once
+  struct Chunk {
+    void* dst;
+    const void* src;
+    size_t bytes;
+    int field;
+    bool last;
+  };
+  std::vector<Chunk> pend_up, pend_dn;
+  size_t pu = 0, pd = 0;  // next pending chunk
+  size_t chunk_bytes = 0;
   bool known_finite = false;
   long long n_alloc = 0;  // (im+3)*si
   long long n_py = 0;     // (im+2)*si : the Python-visible array
@@ -581,7 +615,8 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
   if (rc) return rc;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  if (mode == MODE_SYNC) {  // (every inflow word read in one round: host reads are slow under bulk copies)
+  if (mode == MODE_SYNC && !inflow_by_arg(h->g.km)) {  // (else k_step_head_arg before each launch)
+    // (every inflow word read in one round: host reads are slow under bulk copies)
     const int n_in = 3 * h->g.km, nt = std::min(1024, (n_in + 31) / 32 * 32);
     k_step_head<<<1, nt, 0, h->st>>>(h->inflow_d, h->inflow_h, n_in, h->book_d);
   }
@@ -885,7 +920,55 @@ static int ensure_copy_streams(lesb_domain* h) {
   for (cudaEvent_t* e : {&h->ev_up, &h->ev_commit, &h->ev_snap})
     CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (cudaEvent_t& e : h->ev_dn) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const char* mb = std::getenv("LESB_COPY_CHUNK_MB");  // 0: every copy enqueued at once
+  h->chunk_bytes = (size_t)((mb ? std::atof(mb) : 8.0) * (1 << 20));
   return LESB_OK;
+}
+
+static int enqueue_chunk(lesb_domain* h, bool up) {
+  auto& q = up ? h->pend_up : h->pend_dn;
+  size_t& i = up ? h->pu : h->pd;
+  const lesb_domain::Chunk c = q[i++];
+  if (i == q.size()) {
+    q.clear();
+    i = 0;
+  }
+  if (!c.dst) return LESB_OK;  // (superseded)
+  CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                     up ? h->up_st : h->dn_st));
+  if (!up && c.last) CK(cudaEventRecord(h->ev_dn[c.field], h->dn_st));
+  return LESB_OK;
+}
+
+static int flush_copies(lesb_domain* h, bool up) {
+  while (!(up ? h->pend_up : h->pend_dn).empty()) {
+    int rc = enqueue_chunk(h, up);
+    if (rc) return rc;
+  }
+  return LESB_OK;
+}
+
+// one chunk of each direction (after a step's launch)
+static int pump_copies(lesb_domain* h) {
+  for (bool up : {true, false}) {
+    auto& q = up ? h->pend_up : h->pend_dn;
+    size_t done = 0;
+    while (!q.empty() && done < h->chunk_bytes) {
+      done += q[up ? h->pu : h->pd].bytes;
+      int rc = enqueue_chunk(h, up);
+      if (rc) return rc;
+    }
+  }
+  return LESB_OK;
+}
+
+static void split_copy(lesb_domain* h, bool up, void* dst, const void* src, size_t bytes, int field) {
+  auto& q = up ? h->pend_up : h->pend_dn;
+  const size_t cb = h->chunk_bytes ? h->chunk_bytes : bytes;
+  for (size_t off = 0; off < bytes; off += cb) {
+    const size_t n = std::min(cb, bytes - off);
+    q.push_back({(char*)dst + off, (const char*)src + off, n, field, off + n == bytes});
+  }
 }
 
 int lesb_stage_upload(lesb_handle h, int field, const float* host) {
@@ -898,9 +981,12 @@ int lesb_stage_upload(lesb_handle h, int field, const float* host) {
   const size_t bytes = field_count(h, field) * sizeof(float);
   if (!h->staged[field]) CK(cudaMalloc(&h->staged[field], bytes));
   CK(cudaStreamWaitEvent(h->up_st, h->ev_commit, 0));  // the last commit has read the staging buffer
-  CK(cudaMemcpyAsync(h->staged[field], host, bytes, cudaMemcpyHostToDevice, h->up_st));
+  for (size_t q = h->pu; q < h->pend_up.size(); ++q)      // a pending copy into this buffer is superseded
+    if (h->pend_up[q].field == field) h->pend_up[q].dst = nullptr;
+  split_copy(h, true, h->staged[field], host, bytes, field);
+  if (!h->chunk_bytes) rc = flush_copies(h, true);
   h->staged_mask |= 1u << field;
-  return LESB_OK;
+  return rc;
 }
 
 int lesb_stage_commit(lesb_handle h) {
@@ -908,6 +994,8 @@ int lesb_stage_commit(lesb_handle h) {
   std::lock_guard<std::mutex> lk(h->mu);
   CK(cudaSetDevice(h->device));
   if (!h->staged_mask) return LESB_OK;
+  int rc = flush_copies(h, true);
+  if (rc) return rc;
   CK(cudaEventRecord(h->ev_up, h->up_st));
   CK(cudaStreamWaitEvent(h->st, h->ev_up, 0));
   for (int f = 0; f < 8; ++f) {
@@ -930,19 +1018,29 @@ int lesb_download_async(lesb_handle h, int field, float* host) {
   if (rc) return rc;
   const size_t bytes = field_count(h, field) * sizeof(float);
   if (!h->snap[field]) CK(cudaMalloc(&h->snap[field], bytes));
+  for (size_t q = h->pd; q < h->pend_dn.size(); ++q)  // this snapshot buffer still has copies pending
+    if (h->pend_dn[q].field == field) {
+      rc = flush_copies(h, false);
+      if (rc) return rc;
+      break;
+    }
   CK(cudaStreamWaitEvent(h->st, h->ev_dn[field], 0));  // the last download has read this snapshot buffer
   CK(copy_field(h->snap[field], d, field_count(h, field), h->device, h->st));
   CK(cudaEventRecord(h->ev_snap, h->st));
-  CK(cudaStreamWaitEvent(h->dn_st, h->ev_snap, 0));
-  CK(cudaMemcpyAsync(host, h->snap[field], bytes, cudaMemcpyDeviceToHost, h->dn_st));
-  CK(cudaEventRecord(h->ev_dn[field], h->dn_st));
-  return LESB_OK;
+  CK(cudaStreamWaitEvent(h->dn_st, h->ev_snap, 0));  // (ahead of every chunk queued from now on)
+  split_copy(h, false, host, h->snap[field], bytes, field);
+  if (!h->chunk_bytes) rc = flush_copies(h, false);
+  return rc;
 }
 
 int lesb_copies_wait(lesb_handle h) {
   if (!h) return fail(LESB_E_ARG, "null handle");
   std::lock_guard<std::mutex> lk(h->mu);
   CK(cudaSetDevice(h->device));
+  for (bool up : {true, false}) {
+    int rc = flush_copies(h, up);
+    if (rc) return rc;
+  }
   if (h->up_st) CK(cudaStreamSynchronize(h->up_st));
   if (h->dn_st) CK(cudaStreamSynchronize(h->dn_st));
   return LESB_OK;
@@ -1117,7 +1215,17 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   std::memcpy(h->inflow_h, in_u, km * sizeof(float));
   std::memcpy(h->inflow_h + km, in_v, km * sizeof(float));
   std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
+  if (inflow_by_arg(km)) {
+    InflowArg arg;
+    std::memcpy(arg.v, h->inflow_h, 3 * km * sizeof(float));
+    k_step_head_arg<<<1, std::min(1024, (3 * km + 31) / 32 * 32), 0, h->st>>>(h->inflow_d, arg, 3 * km, h->book_d);
+    CK(cudaGetLastError());
+  }
   CK(cudaGraphLaunch(ge, h->st));
+  if (h->up_st) {
+    rc = pump_copies(h);
+    if (rc) return rc;
+  }
   CK(cudaStreamSynchronize(h->st));
   if (residuals_out && h->link.comm) {  // C4: the global residual history
     rc = nccl_residuals(h, n_iter);

@@ -79,12 +79,18 @@ def test_stage_argument_errors():
     fs.commit_staged()  # nothing staged: no-op
 
 
-def test_pipelined_windows_match_synchronous():
+@pytest.mark.parametrize("chunk_mb", [None, "0.03", "0"])
+def test_pipelined_windows_match_synchronous(monkeypatch, chunk_mb):
     """bench.py's e2e pattern at 64x48x32 with buildings: the next window's
     initial state staged during the current window, each window's fields
     downloaded asynchronously while the next runs -- against the same
-    windows run with assignment and synchronous reads."""
+    windows run with assignment and synchronous reads.  Copies in the
+    default chunks (one per field here), in 30 KB chunks (many per field,
+    pumped one per step, the rest flushed by commit / wait) and unchunked."""
     import paper_1504_02264_b200 as P
+
+    if chunk_mb is not None:
+        monkeypatch.setenv("LESB_COPY_CHUNK_MB", chunk_mb)
 
     st = gi.config2_state(64, 48, 32)
     rng = np.random.default_rng(5)
