@@ -126,13 +126,29 @@ __global__ void k_velnw_bondv1(Geo g_in, Spac s, const float* __restrict__ u, co
   unsigned bits = 0;
   if (k <= g.km + 1 && j <= g.jm + 1) {
     long long c = cidx(g, i, j, k);
-    bool interior = i >= 1 && i <= g.im && j >= 1 && j <= g.jm && k >= 1 && k <= g.km;
-    if (interior) {
-      float a = velnw_u<P2>(g, s, u, p, fgh, dt, c, i);
-      float b = velnw_v<P2>(g, s, v, p, fgh, dt, c, j);
-      float d = velnw_w<P2>(g, s, w, p, fgh, dt, c, k);
-      if (!(finite32(a) && finite32(b) && finite32(d))) bits |= F_VELNW;
-      ub[c] = a; vb[c] = b; wb[c] = d;
+    // a warp is a run of k in one (i, j) column (box_launch: blockDim.x a
+    // multiple of 32), so this test is warp uniform
+    const bool column = i >= 1 && i <= g.im && j >= 1 && j <= g.jm;
+    if (column) {
+      // every k of an interior column, k halo included, on one path (the
+      // halo lanes at k = 0 and km + 1 share a warp with interior lanes: a
+      // branch per cell made those warps run both paths).  bondv1 there
+      // (les.py:254-258): u, v = velnw at the clamped k, w = 0; velnw's own
+      // check covers its w face at k = 0 (les.py:413-415, in_velnw_w).
+      const int kb = k < 1 ? 1 : (k > g.km ? g.km : k);
+      const int kw = k > g.km ? g.km : k;
+      const float a = velnw_u<P2>(g, s, u, p, fgh, dt, c + (kb - k), i);
+      const float b = velnw_v<P2>(g, s, v, p, fgh, dt, c + (kb - k), j);
+      const float d = velnw_w<P2>(g, s, w, p, fgh, dt, c + (kw - k), kw);
+      const bool kh = k == 0 || k == g.km + 1;
+      const bool ab = finite32(a) && finite32(b);
+      if (!kh) {
+        if (!(ab && finite32(d))) bits |= F_VELNW;
+      } else {
+        if (k == 0 && !finite32(d)) bits |= F_VELNW;
+        if (!ab) bits |= F_BONDV1;
+      }
+      ub[c] = a; vb[c] = b; wb[c] = kh ? 0.0f : d;
     } else {
       // velnw's own writes to halo faces are overwritten by bondv1 but are
       // still checked after the velnw stage (les.py:413-415).
