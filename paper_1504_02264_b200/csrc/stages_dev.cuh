@@ -445,13 +445,14 @@ __global__ void __launch_bounds__(128, FUSED_MINB) k_fused_rhs(Geo g_in, Spac s,
   if (k <= g.km + 1 && j <= g.jm + 1) {
     long long c = cidx(g, i, j, k);
     bool interior = i >= 1 && i <= g.im && j >= 1 && j <= g.jm && k >= 1 && k <= g.km;
+    // adam and the stores are common to interior and halo cells (a warp's
+    // k-halo lanes share it with interior lanes: only the loads differ)
+    float fo[3], f[3], vk[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) fo[a] = fgh_old[3 * c + a];
     if (interior) {
       // the last-used operands first: their DRAM latency overlaps velfg / les
       const float m = mask[c];
-      float fo[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) fo[a] = fgh_old[3 * c + a];
-      float f[3];
       f[0] = velfg_point<0, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       f[1] = velfg_point<1, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
       f[2] = velfg_point<2, P2>(g, s, ub, vb, wb, vn, c, i, j, k);
@@ -460,7 +461,6 @@ __global__ void __launch_bounds__(128, FUSED_MINB) k_fused_rhs(Geo g_in, Spac s,
       const float coef = (P2 && s.dtp2) ? m * s.rdt : m / dt;
       const float keep = 1.0f - m;
       const float vel[3] = {ub[c], vb[c], wb[c]};
-      float vk[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         f[a] = f[a] - coef * vel[a];
@@ -478,36 +478,32 @@ __global__ void __launch_bounds__(128, FUSED_MINB) k_fused_rhs(Geo g_in, Spac s,
         for (int a = 0; a < 3; ++a) f[a] = f[a] + add[a];
         if (!(finite32(f[0]) && finite32(f[1]) && finite32(f[2]))) bits |= F_LES;
       }
-      // adam
-      float nf[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        nf[a] = 1.5f * f[a] - 0.5f * fo[a];
-      }
-      if (!(finite32(nf[0]) && finite32(nf[1]) && finite32(nf[2]))) bits |= F_ADAM;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        fgh[3 * c + a] = nf[a];
-        fgh_old[3 * c + a] = f[a];
-      }
-      ua[c] = vk[0]; va[c] = vk[1]; wa[c] = vk[2];
       // divergence of the post-feedbf velocities, / dt
       const float um = rd(0, c - g.si, i - 1, 0);
       const float vm_ = rd(1, c - g.sj, i, j - 1 < 1);
       const float wm = rd(2, c - 1, i, k - 1 < 1);
       const float dv = div_point<P2>(g, s, vk[0], um, vk[1], vm_, vk[2], wm, i, j, k);
       rhs[c] = (P2 && s.dtp2) ? dv * s.rdt : dv / dt;
-    } else if (i <= g.im + 1) {
-      ua[c] = ub[c]; va[c] = vb[c]; wa[c] = wb[c];
+    } else {
+      // halo: velfg / feedbf / les leave fgh and the velocities as they are;
+      // adam runs on the whole array (les.py:323-327)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const float x = fgh[3 * c + a];
-        const float y = 1.5f * x - 0.5f * fgh_old[3 * c + a];
-        if (!finite32(y)) bits |= F_ADAM;
-        fgh[3 * c + a] = y;
-        fgh_old[3 * c + a] = x;
-      }
+      for (int a = 0; a < 3; ++a) f[a] = fgh[3 * c + a];
+      vk[0] = ub[c];
+      vk[1] = vb[c];
+      vk[2] = wb[c];
     }
+    // adam
+    float nf[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) nf[a] = 1.5f * f[a] - 0.5f * fo[a];
+    if (!(finite32(nf[0]) && finite32(nf[1]) && finite32(nf[2]))) bits |= F_ADAM;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      fgh[3 * c + a] = nf[a];
+      fgh_old[3 * c + a] = f[a];
+    }
+    ua[c] = vk[0]; va[c] = vk[1]; wa[c] = vk[2];
   }
   flag_or(flags, bits);
 }
