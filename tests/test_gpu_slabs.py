@@ -3,6 +3,10 @@ halo-plane copies (lesb_group_step) must reproduce the single-domain step
 bitwise for every field (halos included), report the same blow-up step and
 stage, and give the same residuals to summation-order tolerance."""
 
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -105,3 +109,17 @@ def test_slabs_config1_blowup():
         assert err.value.stage == "velfg"
     finally:
         grp.close()
+
+
+def test_slabs_runtime_specialised():
+    """The slab group tests with every kernel compiled for its geometry at run
+    time (LESB_JIT_MIN_CELLS=0, fresh process): the slabs of a group share
+    one specialised resident kernel (same shape and tile plan), and slabs
+    launched one by one must not wait on a neighbour whose kernel is still
+    being compiled (measured: slab positions as compile-time constants gave
+    each slab its own kernel and the "separate" launches timed out)."""
+    env = dict(os.environ, LESB_JIT_MIN_CELLS="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "equal_single_domain and (resident or separate or serial)"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
