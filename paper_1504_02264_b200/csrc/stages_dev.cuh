@@ -271,6 +271,10 @@ __global__ void k_feedbf(Geo g, float* __restrict__ u, float* __restrict__ v, fl
 struct PlainReader {
   const float* V[3];
   __device__ __forceinline__ float operator()(int m, long long q, int, int) const { return V[m][q]; }
+  __device__ __forceinline__ void all(long long q, int, int, float out[3]) const {
+#pragma unroll
+    for (int m = 0; m < 3; ++m) out[m] = V[m][q];
+  }
 };
 
 // feedbf masks interior cells only (les.py:281-282); halo cells keep their
@@ -285,6 +289,17 @@ struct MaskedReader {
     float x = V[m][q];
     return interior ? x * (1.0f - mask[q]) : x;
   }
+  // the three components at one cell: one mask load and one 1 - mask (the
+  // compiler did not merge them across three operator() calls)
+  __device__ __forceinline__ void all(long long q, int iq, int on_axis_halo, float out[3]) const {
+    const bool interior = !on_axis_halo && (iq >= 1 || !g.west_bc) && (iq <= g.im || !g.east_bc);
+    const float keep = interior ? 1.0f - mask[q] : 0.0f;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const float x = V[m][q];
+      out[m] = interior ? x * keep : x;
+    }
+  }
 };
 
 template <class R, bool P2 = false>
@@ -293,15 +308,25 @@ __device__ __forceinline__ void les_point(const Geo& g, const Spac& s, const R& 
   // neighbour reads: (m, axis, +/-).  on_axis_halo marks a j or k halo cell.
   float d[3][3];
   float ctr[3], nb_hi[3][3], nb_lo[3][3];
+  {
+    float t[7][3];
+    rd.all(c, i, 0, t[0]);
+    rd.all(c + g.si, i + 1, 0, t[1]);
+    rd.all(c - g.si, i - 1, 0, t[2]);
+    rd.all(c + g.sj, i, j + 1 > g.jm, t[3]);
+    rd.all(c - g.sj, i, j - 1 < 1, t[4]);
+    rd.all(c + 1, i, k + 1 > g.km, t[5]);
+    rd.all(c - 1, i, k - 1 < 1, t[6]);
 #pragma unroll
-  for (int m = 0; m < 3; ++m) {
-    ctr[m] = rd(m, c, i, 0);
-    nb_hi[m][0] = rd(m, c + g.si, i + 1, 0);
-    nb_lo[m][0] = rd(m, c - g.si, i - 1, 0);
-    nb_hi[m][1] = rd(m, c + g.sj, i, j + 1 > g.jm);
-    nb_lo[m][1] = rd(m, c - g.sj, i, j - 1 < 1);
-    nb_hi[m][2] = rd(m, c + 1, i, k + 1 > g.km);
-    nb_lo[m][2] = rd(m, c - 1, i, k - 1 < 1);
+    for (int m = 0; m < 3; ++m) {
+      ctr[m] = t[0][m];
+      nb_hi[m][0] = t[1][m];
+      nb_lo[m][0] = t[2][m];
+      nb_hi[m][1] = t[3][m];
+      nb_lo[m][1] = t[4][m];
+      nb_hi[m][2] = t[5][m];
+      nb_lo[m][2] = t[6][m];
+    }
   }
   const float hx = s.dx1[i], hy = s.dy1[j], hz = s.dzn[k];
   const float den[3] = {hx + s.dx1[i + 1], hy + s.dy1[j + 1], hz + s.dzn[k + 1]};
