@@ -1040,13 +1040,27 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
       // column itself, with the press k halo (p[0] = p[1], p[km+1] = 0)
       float* dst = a.p + cidx(g, i, j, 0);
       const int c0 = colour(i + g.ioff, j, 0);
-      for (int k = lane; k <= km + 1; k += 32) {
-        const int kr = k == 0 ? 1 : (k > km ? km : k);
-        const float v = S[cb + (c0 ^ (kr & 1)) * KK + (kr >> 1)];
-        const bool own = k >= 1 && k <= km;
-        if (own && !finite32(v)) bad = F_PRESS;
-        if (own) dst[k] = v;
-        else if (PRESS) dst[k] = (k == km + 1) ? 0.0f : v;
+      // a column's shared-memory reads first, then its stores (one round of
+      // read latency per column instead of one per 32 cells)
+      constexpr int WB = 4;
+      for (int k0 = 0; k0 <= km + 1; k0 += 32 * WB) {
+        float vv[WB];
+#pragma unroll
+        for (int r = 0; r < WB; ++r) {
+          const int k = k0 + lane + 32 * r;
+          const int kr = k == 0 ? 1 : (k > km ? km : k);
+          vv[r] = k <= km + 1 ? S[cb + (c0 ^ (kr & 1)) * KK + (kr >> 1)] : 0.0f;
+        }
+#pragma unroll
+        for (int r = 0; r < WB; ++r) {
+          const int k = k0 + lane + 32 * r;
+          if (k > km + 1) continue;
+          const float v = vv[r];
+          const bool own = k >= 1 && k <= km;
+          if (own && !finite32(v)) bad = F_PRESS;
+          if (own) dst[k] = v;
+          else if (PRESS) dst[k] = (k == km + 1) ? 0.0f : v;
+        }
       }
     } else {
       for (int k = lane; k <= km + 1; k += 32) {
