@@ -94,7 +94,7 @@ __global__ void k_step_head(float* __restrict__ in_d, const float* __restrict__ 
 // the inflow as a kernel argument (launched before the step graph): the step
 // then reads nothing from host memory -- a host read waits behind a bulk
 // device-to-host copy's writes on the link
-constexpr int INFLOW_ARG_MAX = 960;  // (3 km floats, within the 4 KB parameter space)
+constexpr int INFLOW_ARG_MAX = 288;  // (3 km floats, km <= 96; the argument is rewritten every step)
 struct InflowArg {
   float v[INFLOW_ARG_MAX];
 };
@@ -183,6 +183,10 @@ struct lesb_domain {
   int res_cap = 0;
   float* scratch = nullptr;  // im*jm*km
   std::map<std::tuple<int, int, int, unsigned>, cudaGraphExec_t> graphs;
+  // synchronous step graphs with the inflow as a kernel argument: the head
+  // node (its arguments set before every launch) and the captured graph it
+  // belongs to
+  std::map<std::tuple<int, int, int, unsigned>, std::pair<cudaGraph_t, cudaGraphNode_t>> heads;
   bool timing = false;
   int sor_path = 0;  // 0 auto, 1 streaming colour passes, 2 shared-memory-resident solver, 3 natural-layout passes
   float* split = nullptr;  // colour-split p / rhs of the streaming red-black passes (4 * SplitGeo::n floats)
@@ -451,6 +455,8 @@ int check_resident_err(lesb_domain* h) {
 void clear_graphs(lesb_domain* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
+  for (auto& kv : h->heads) cudaGraphDestroy(kv.second.first);
+  h->heads.clear();
 }
 
 float* field_ptr(lesb_domain* h, int f) {
@@ -602,23 +608,32 @@ cudaError_t enqueue_step_body(lesb_domain* h, int n_iter, int scheme, float omeg
   return e;
 }
 
-int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cudaGraphExec_t* out) {
+int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cudaGraphExec_t* out,
+              cudaGraphNode_t* head = nullptr) {
   unsigned ob;
   std::memcpy(&ob, &omega, 4);
   auto key = std::make_tuple(mode | (h->timing ? 2 : 0), n_iter, scheme, ob);
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) {
     *out = it->second;
+    if (head) {
+      auto hn = h->heads.find(key);
+      *head = hn == h->heads.end() ? nullptr : hn->second.second;
+    }
     return LESB_OK;
   }
+  const bool arg_head = mode == MODE_SYNC && inflow_by_arg(h->g.km);
   int rc = ensure_partials(h, n_iter);
   if (rc) return rc;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-  if (mode == MODE_SYNC && !inflow_by_arg(h->g.km)) {  // (else k_step_head_arg before each launch)
+  const int n_in = 3 * h->g.km, nt_in = std::min(1024, (n_in + 31) / 32 * 32);
+  if (arg_head) {  // (its arguments are set before every launch: lesb_step)
+    static const InflowArg zero{};
+    k_step_head_arg<<<1, nt_in, 0, h->st>>>(h->inflow_d, zero, n_in, h->book_d);
+  } else if (mode == MODE_SYNC) {
     // (every inflow word read in one round: host reads are slow under bulk copies)
-    const int n_in = 3 * h->g.km, nt = std::min(1024, (n_in + 31) / 32 * 32);
-    k_step_head<<<1, nt, 0, h->st>>>(h->inflow_d, h->inflow_h, n_in, h->book_d);
+    k_step_head<<<1, nt_in, 0, h->st>>>(h->inflow_d, h->inflow_h, n_in, h->book_d);
   }
   bool tail_done = false;
   cudaError_t body_err =
@@ -635,12 +650,34 @@ int get_graph(lesb_domain* h, int mode, int n_iter, int scheme, float omega, cud
     return fail(LESB_E_CUDA, std::string("step capture: ") + cudaGetErrorString(body_err));
   }
   if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  cudaGraphNode_t head_node = nullptr;
+  if (arg_head) {
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      cudaKernelNodeParams kp;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel &&
+          cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == (void*)k_step_head_arg) {
+        head_node = nd;
+        break;
+      }
+    }
+    if (!head_node) {
+      cudaGraphDestroy(graph);
+      return fail(LESB_E_CUDA, "step capture: inflow node not found");
+    }
+  }
   cudaGraphExec_t exec;
   e = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
+  if (arg_head && e == cudaSuccess) h->heads[key] = {graph, head_node};
+  else cudaGraphDestroy(graph);
   if (e != cudaSuccess) return fail(LESB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   h->graphs[key] = exec;
   *out = exec;
+  if (head) *head = head_node;
   return LESB_OK;
 }
 
@@ -1209,17 +1246,24 @@ int lesb_step(lesb_handle h, const float* in_u, const float* in_v, const float* 
   if (rc) return rc;
   if (failed) return LESB_NONFINITE;
   cudaGraphExec_t ge;
-  rc = get_graph(h, MODE_SYNC, n_iter, scheme, omega, &ge);
+  cudaGraphNode_t head = nullptr;
+  rc = get_graph(h, MODE_SYNC, n_iter, scheme, omega, &ge, &head);
   if (rc) return rc;
   const int km = h->g.km;
   std::memcpy(h->inflow_h, in_u, km * sizeof(float));
   std::memcpy(h->inflow_h + km, in_v, km * sizeof(float));
   std::memcpy(h->inflow_h + 2 * km, in_w, km * sizeof(float));
-  if (inflow_by_arg(km)) {
+  if (head) {  // the inflow as the head node's argument (no host read in the step)
     InflowArg arg;
     std::memcpy(arg.v, h->inflow_h, 3 * km * sizeof(float));
-    k_step_head_arg<<<1, std::min(1024, (3 * km + 31) / 32 * 32), 0, h->st>>>(h->inflow_d, arg, 3 * km, h->book_d);
-    CK(cudaGetLastError());
+    int n_in = 3 * km;
+    void* args[] = {&h->inflow_d, &arg, &n_in, &h->book_d};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)k_step_head_arg;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(std::min(1024, (n_in + 31) / 32 * 32));
+    kp.kernelParams = args;
+    CK(cudaGraphExecKernelNodeSetParams(ge, head, &kp));
   }
   CK(cudaGraphLaunch(ge, h->st));
   if (h->up_st) {
