@@ -141,6 +141,15 @@ cudaKernel_t compile(const std::string& src, const std::string& expr) {
   std::vector<char> bin(nbin);
   nv.cubin(prog, bin.data());
   nv.destroy(&prog);
+  // LESB_JIT_DUMP=<dir>: keep each specialised cubin (profiling: nvdisasm -g maps
+  // an ncu source page of the specialised kernel back to the device source)
+  if (const char* dir = std::getenv("LESB_JIT_DUMP")) {
+    const std::string path = std::string(dir) + "/" + sym + ".cubin";
+    if (FILE* f = std::fopen(path.c_str(), "wb")) {
+      std::fwrite(bin.data(), 1, bin.size(), f);
+      std::fclose(f);
+    }
+  }
   cudaLibrary_t lib;
   if (sym.empty() || cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
     cudaGetLastError();

@@ -672,6 +672,12 @@ struct ResGroup {
   int tps;  // tiles per slab
 };
 
+// a receive that finds a neighbour's word not yet published waits this many
+// ns before reading it again (0: spin)
+#ifndef RES_SPIN_NS
+#define RES_SPIN_NS 0
+#endif
+
 template <bool PRESS, bool SLAB>
 __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_constant__ ResGroup grp) {
   extern __shared__ float smem[];
@@ -953,6 +959,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
               atomicOr(a.err, 1u);
               timed_out = true;
             }
+            if (RES_SPIN_NS) __nanosleep(RES_SPIN_NS);  // (leave the issue slots to warps still updating)
             const unsigned long long* src = (w2 ? XB2 : XB1) + roff[u] + h;
             v[u][h] = (SLAB && ((rsys >> u) & 1u)) ? ld_ll_sys(src) : ld_ll(src);
           }
@@ -988,6 +995,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_sor_resident(const __grid_co
               atomicOr(a.err, 1u);
               timed_out = true;
             }
+            if (RES_SPIN_NS) __nanosleep(RES_SPIN_NS);
             x = (SLAB && (e.z & 2)) ? ld_ll_sys(src) : ld_ll(src);
           }
           Sd[e.x + sl] = __uint_as_float((unsigned)x);
